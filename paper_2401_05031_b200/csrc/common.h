@@ -1,0 +1,78 @@
+// Host+device shared definitions for the tokadapt CUDA library.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/tokadapt_cuda.h"
+
+namespace ta {
+
+// Fused GEMM epilogues.  All GEMMs are C[m, n] = sum_k A[m, k] * W[n, k] (nn.Linear
+// layout, both operands K-major) followed by one of these.
+enum EpiKind : int {
+  EPI_BIAS = 0,        // out(act dtype) = acc + bias
+  EPI_BIAS_GELU = 1,   // out(act dtype) = gelu_erf(acc + bias)
+  EPI_BIAS_RESID = 2,  // out(fp32)      = resid[m] + acc + bias   (residual stream update)
+  EPI_PATCH = 3,       // out(fp32)      = acc + bias + pos[row]   (patch embedding)
+};
+
+struct GemmEpi {
+  const float* bias = nullptr;   // [N]
+  const float* resid = nullptr;  // fp32 [M, N], row m of the *input* numbering
+  const float* pos = nullptr;    // EPI_PATCH: positional table [*, N], row = row_off + m % rows_in
+  void* out = nullptr;           // row-major, row stride N
+  // Output row remap: out_row(m) = (m / rows_in) * rows_out + row_off + m % rows_in.
+  // rows_in == 0 means identity.  This is how prompt rows are reserved per image
+  // (accumulate mode) and how patch rows land after the cls row, without copies.
+  int rows_in = 0;
+  int rows_out = 0;
+  int row_off = 0;
+};
+
+__host__ __device__ inline long long epi_out_row(const GemmEpi& e, long long m) {
+  if (e.rows_in == 0) return m;
+  const long long b = m / e.rows_in;
+  return b * e.rows_out + e.row_off + (m - b * e.rows_in);
+}
+
+// Library status codes (mirrored in include/tokadapt_cuda.h).
+int set_last_cuda_error(cudaError_t e);
+
+int device_sm_count();
+
+struct HeadDesc {
+  const float* w;  // [classes, D]
+  const float* b;  // [classes]
+  int classes;
+};
+
+// Launchers (gemm.cu)
+int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, bool out_bf16,
+              const GemmEpi& epi, cudaStream_t stream);
+int gemm_f32(const float* A, const float* W, int M, int N, int K, int epi_kind,
+             const GemmEpi& epi, cudaStream_t stream);
+
+// rowops.cu
+int patchify(const float* img, void* out, int B, int S, int P, int Kp, int dtype, cudaStream_t s);
+int insert_rows(float* x, int B, int t_total, int D, const float* cls, const float* pos,
+                const float* const* prompt_tab, const int32_t* task_ids, int layer, int gamma,
+                int prompt_row, cudaStream_t s);
+int layernorm(const float* x, const float* w, const float* b, void* out, int rows, int D,
+              int out_dtype, cudaStream_t s);
+int head(const float* x, int B, int t_total, int D, const float* nw, const float* nb,
+         const HeadDesc* heads, const int32_t* task, float* logits, int c_max, cudaStream_t s);
+
+// tome.cu.  metric source: either fp32 [B, t, c] (metric != null) or the k third of a
+// qkv activation [B, t, 3*H*c] in `qkv_dtype`, averaged over heads (ToMe k.mean(1)).
+int match(const float* metric, const void* qkv, int qkv_dtype, int B, int t, int heads, int c,
+          int r, int32_t* src, int32_t* dst, int32_t* unm, cudaStream_t s);
+int merge(const float* x, const float* size, int B, int t, int D, int r, const int32_t* src,
+          const int32_t* dst, const int32_t* unm, const float* ln_w, const float* ln_b,
+          float* x_out, float* size_out, void* h_out, int h_dtype, cudaStream_t s);
+
+// attention.cu
+int attention(const void* qkv, const float* size, int B, int t, int H, int hd, void* out,
+              int dtype, cudaStream_t s);
+
+}  // namespace ta

@@ -1,0 +1,511 @@
+// Token-adapted ViT forward and the C ABI of
+// include/tokadapt_cuda.h.
+//
+// One call of ta_forward runs, for a batch at one gamma:
+//   patchify -> patch GEMM (+bias +pos, rows placed after cls / before prompts)
+//   -> cls / prompt rows -> L x [ prompts, LN1, QKV GEMM, attention(+log size),
+//      proj GEMM (+residual), (match, merge+LN2) | LN2, fc1 GEMM (+GELU),
+//      fc2 GEMM (+residual, rows re-strided for next-layer prompts) ]
+//   -> final LN on cls + per-task head.
+// The per-layer token count t_l is static per (model, gamma); all buffers live in the
+// caller's workspace, so the whole call is CUDA-graph capturable.
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "common.h"
+
+namespace ta {
+
+static thread_local int g_last_cuda_error = 0;
+int set_last_cuda_error(cudaError_t e) {
+  g_last_cuda_error = static_cast<int>(e);
+  return TA_ERR_CUDA;
+}
+
+int device_sm_count() {
+  static int count = 0;
+  if (count == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev);
+    if (count <= 0) count = 148;
+  }
+  return count;
+}
+
+static int check_arch(int device) {
+  int major = 0, minor = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  if (e != cudaSuccess) return set_last_cuda_error(e);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+  return (major == 10 && minor == 0) ? TA_OK : TA_ERR_ARCH;
+}
+
+}  // namespace ta
+
+using namespace ta;
+
+struct ta_model {
+  int device = 0;
+  ta_model_desc d{};
+  int hd = 0, grid = 0, n_patches = 0, n_tokens = 0, kp = 0;
+  bool has_weights = false;
+  ta_weights w{};
+  std::vector<ta_layer_weights> layers;
+  std::vector<HeadDesc> heads;  // host copy
+  HeadDesc* heads_dev = nullptr;
+  std::map<int, std::vector<const float*>> prompts;  // gamma -> per-task pointer
+  std::map<int, const float**> prompt_tab;             // gamma -> device table [n_tasks]
+  // ta_forward_host cache
+  void* host_ws = nullptr;
+  size_t host_ws_bytes = 0;
+  std::mutex host_mu;
+};
+
+namespace {
+
+struct Schedule {
+  std::vector<int> t, r;
+  int t_max = 0, t_final = 0;
+};
+
+Schedule make_schedule(const ta_model* m, int gamma) {
+  Schedule s;
+  const int L = m->d.depth, N = m->n_tokens;
+  int t = N;
+  for (int l = 0; l < L; ++l) {
+    int tl, rl = 0;
+    if (gamma > 0) {
+      tl = m->d.prompt_mode == TA_PROMPT_ACCUMULATE ? N + gamma * (l + 1) : N + gamma;
+    } else {
+      tl = t;
+      if (gamma < 0) rl = std::min(-gamma, (tl - 1) / 2);
+      if (rl < 0) rl = 0;
+    }
+    s.t.push_back(tl);
+    s.r.push_back(rl);
+    s.t_max = std::max(s.t_max, tl);
+    t = tl - rl;
+  }
+  s.t_final = t;
+  return s;
+}
+
+size_t align_up(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
+
+struct Workspace {
+  void* patches;
+  float* x[2];
+  void* h;
+  void* qkv;
+  void* attn;
+  void* mlp;
+  float* size[2];
+  int32_t* src;
+  int32_t* dst;
+  int32_t* unm;
+  size_t total;
+};
+
+Workspace carve(const ta_model* m, int B, const Schedule& s, char* base) {
+  const size_t A = m->d.dtype == TA_DTYPE_BF16 ? 2 : 4;
+  const size_t D = m->d.dim, rows = static_cast<size_t>(B) * s.t_max;
+  Workspace w{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* p = base ? base + off : nullptr;
+    off += align_up(bytes);
+    return p;
+  };
+  w.patches = take(static_cast<size_t>(B) * m->n_patches * m->kp * A);
+  w.x[0] = reinterpret_cast<float*>(take(rows * D * 4));
+  w.x[1] = reinterpret_cast<float*>(take(rows * D * 4));
+  w.h = take(rows * D * A);
+  w.qkv = take(rows * 3 * D * A);
+  w.attn = take(rows * D * A);
+  w.mlp = take(rows * m->d.mlp_dim * A);
+  w.size[0] = reinterpret_cast<float*>(take(rows * 4));
+  w.size[1] = reinterpret_cast<float*>(take(rows * 4));
+  w.src = reinterpret_cast<int32_t*>(take(rows * 4));
+  w.dst = reinterpret_cast<int32_t*>(take(rows * 4));
+  w.unm = reinterpret_cast<int32_t*>(take(rows * 4));
+  w.total = off;
+  return w;
+}
+
+int linear(const ta_model* m, const void* a, const void* wt, int M, int N, int K, int epi_kind,
+           const GemmEpi& epi, cudaStream_t st) {
+  if (m->d.dtype == TA_DTYPE_BF16)
+    return gemm_bf16(a, wt, M, N, K, epi_kind, epi_kind == EPI_BIAS || epi_kind == EPI_BIAS_GELU,
+                     epi, st);
+  return gemm_f32(static_cast<const float*>(a), static_cast<const float*>(wt), M, N, K, epi_kind,
+                  epi, st);
+}
+
+size_t trace_len(const Schedule& s, int B) {
+  size_t n = 0;
+  for (size_t l = 0; l < s.t.size(); ++l)
+    if (s.r[l] > 0) n += static_cast<size_t>(B) * (2 * s.r[l] + (s.t[l] + 1) / 2 - s.r[l]);
+  return n;
+}
+
+}  // namespace
+
+#define TA_TRY(expr)          \
+  do {                        \
+    int _rc = (expr);         \
+    if (_rc != TA_OK) return _rc; \
+  } while (0)
+
+extern "C" {
+#pragma GCC visibility push(default)
+
+int ta_abi_version(void) { return TA_ABI_VERSION; }
+
+const char* ta_strerror(int code) {
+  switch (code) {
+    case TA_OK: return "ok";
+    case TA_ERR_INVALID: return "invalid argument";
+    case TA_ERR_SHAPE: return "unsupported shape or alignment";
+    case TA_ERR_CONFIG: return "inconsistent model description";
+    case TA_ERR_NO_PROMPT: return "no prompts registered for (task, gamma)";
+    case TA_ERR_NO_WEIGHTS: return "weights or task head not set";
+    case TA_ERR_WORKSPACE: return "workspace too small";
+    case TA_ERR_CUDA: return "CUDA error";
+    case TA_ERR_ARCH: return "device is not sm_100 (B200)";
+  }
+  return "unknown error";
+}
+
+int ta_last_cuda_error(void) { return g_last_cuda_error; }
+
+int ta_model_create(int device, const ta_model_desc* desc, ta_model** out) {
+  if (!desc || !out) return TA_ERR_INVALID;
+  const ta_model_desc& d = *desc;
+  if (d.dim <= 0 || d.depth <= 0 || d.depth > 64 || d.heads <= 0 || d.dim % d.heads ||
+      d.patch <= 0 || d.img % d.patch || d.n_tasks <= 0 || d.max_classes <= 0 ||
+      d.mlp_dim <= 0 || (d.dtype != TA_DTYPE_BF16 && d.dtype != TA_DTYPE_F32) ||
+      (d.prompt_mode != TA_PROMPT_ACCUMULATE && d.prompt_mode != TA_PROMPT_REPLACE))
+    return TA_ERR_CONFIG;
+  const int hd = d.dim / d.heads;
+  if (hd != 64 && hd != 80) return TA_ERR_CONFIG;
+  if (d.dim % 256 != 0 || d.mlp_dim % 256 != 0) return TA_ERR_CONFIG;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return set_last_cuda_error(e);
+  TA_TRY(check_arch(device));
+  auto* m = new ta_model();
+  m->device = device;
+  m->d = d;
+  m->hd = hd;
+  m->grid = d.img / d.patch;
+  m->n_patches = m->grid * m->grid;
+  m->n_tokens = m->n_patches + 1;
+  m->kp = (3 * d.patch * d.patch + 63) / 64 * 64;
+  m->heads.assign(d.n_tasks, HeadDesc{nullptr, nullptr, 0});
+  e = cudaMalloc(&m->heads_dev, sizeof(HeadDesc) * d.n_tasks);
+  if (e != cudaSuccess) {
+    delete m;
+    return set_last_cuda_error(e);
+  }
+  cudaMemcpy(m->heads_dev, m->heads.data(), sizeof(HeadDesc) * d.n_tasks, cudaMemcpyHostToDevice);
+  *out = m;
+  return TA_OK;
+}
+
+void ta_model_destroy(ta_model* m) {
+  if (!m) return;
+  cudaSetDevice(m->device);
+  cudaFree(m->heads_dev);
+  for (auto& kv : m->prompt_tab) cudaFree(kv.second);
+  if (m->host_ws) cudaFree(m->host_ws);
+  delete m;
+}
+
+int ta_model_set_weights(ta_model* m, const ta_weights* w) {
+  if (!m || !w || !w->layers || !w->patch_w || !w->patch_b || !w->cls || !w->pos || !w->norm_w ||
+      !w->norm_b)
+    return TA_ERR_INVALID;
+  for (int l = 0; l < m->d.depth; ++l) {
+    const ta_layer_weights& L = w->layers[l];
+    if (!L.ln1_w || !L.ln1_b || !L.qkv_w || !L.qkv_b || !L.proj_w || !L.proj_b || !L.ln2_w ||
+        !L.ln2_b || !L.fc1_w || !L.fc1_b || !L.fc2_w || !L.fc2_b)
+      return TA_ERR_INVALID;
+  }
+  m->w = *w;
+  m->layers.assign(w->layers, w->layers + m->d.depth);
+  m->w.layers = m->layers.data();
+  m->has_weights = true;
+  return TA_OK;
+}
+
+int ta_model_set_head(ta_model* m, int task, const float* w, const float* b, int classes) {
+  if (!m || !w || !b || task < 0 || task >= m->d.n_tasks || classes <= 0 ||
+      classes > m->d.max_classes)
+    return TA_ERR_INVALID;
+  m->heads[task] = HeadDesc{w, b, classes};
+  cudaError_t e = cudaMemcpy(m->heads_dev + task, &m->heads[task], sizeof(HeadDesc),
+                             cudaMemcpyHostToDevice);
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
+int ta_model_set_prompts(ta_model* m, int task, int gamma, const float* prompts) {
+  if (!m || !prompts || task < 0 || task >= m->d.n_tasks || gamma <= 0) return TA_ERR_INVALID;
+  auto& vec = m->prompts[gamma];
+  if (vec.empty()) vec.assign(m->d.n_tasks, nullptr);
+  vec[task] = prompts;
+  const float** tab = nullptr;
+  auto it = m->prompt_tab.find(gamma);
+  if (it == m->prompt_tab.end()) {
+    cudaError_t e = cudaMalloc(&tab, sizeof(float*) * m->d.n_tasks);
+    if (e != cudaSuccess) return set_last_cuda_error(e);
+    m->prompt_tab[gamma] = tab;
+  } else {
+    tab = it->second;
+  }
+  cudaError_t e = cudaMemcpy(tab, vec.data(), sizeof(float*) * m->d.n_tasks, cudaMemcpyHostToDevice);
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
+int ta_token_schedule(const ta_model* m, int gamma, int* t_out, int* r_out) {
+  if (!m || !t_out || !r_out) return TA_ERR_INVALID;
+  Schedule s = make_schedule(m, gamma);
+  std::copy(s.t.begin(), s.t.end(), t_out);
+  std::copy(s.r.begin(), s.r.end(), r_out);
+  return TA_OK;
+}
+
+int ta_merge_trace_len(const ta_model* m, int batch, int gamma, size_t* n) {
+  if (!m || !n || batch <= 0) return TA_ERR_INVALID;
+  *n = trace_len(make_schedule(m, gamma), batch);
+  return TA_OK;
+}
+
+int ta_workspace_size(const ta_model* m, int batch, int gamma, size_t* bytes) {
+  if (!m || !bytes || batch <= 0) return TA_ERR_INVALID;
+  *bytes = carve(m, batch, make_schedule(m, gamma), nullptr).total;
+  return TA_OK;
+}
+
+int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B, int gamma,
+               float* logits, int32_t* merge_trace, const int32_t* forced_trace, void* ws,
+               size_t ws_bytes, void* stream) {
+  if (!m || !images || !task_ids || !logits || !ws || B <= 0) return TA_ERR_INVALID;
+  if (!m->has_weights) return TA_ERR_NO_WEIGHTS;
+  for (int k = 0; k < m->d.n_tasks; ++k)
+    if (!m->heads[k].w) return TA_ERR_NO_WEIGHTS;
+  const float* const* ptab = nullptr;
+  if (gamma > 0) {
+    auto it = m->prompts.find(gamma);
+    if (it == m->prompts.end()) return TA_ERR_NO_PROMPT;
+    for (const float* p : it->second)
+      if (!p) return TA_ERR_NO_PROMPT;
+    ptab = m->prompt_tab[gamma];
+  }
+  if (gamma < -(m->n_tokens - 1)) return TA_ERR_INVALID;
+  const Schedule s = make_schedule(m, gamma);
+  Workspace w = carve(m, B, s, static_cast<char*>(ws));
+  if (ws_bytes < w.total) return TA_ERR_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const ta_model_desc& d = m->d;
+  const int D = d.dim, L = d.depth, N = m->n_tokens;
+  const int act = d.dtype;
+  const bool accumulate = d.prompt_mode == TA_PROMPT_ACCUMULATE;
+
+  // ---- patch embedding + cls + layer-0 prompts
+  TA_TRY(patchify(images, w.patches, B, d.img, d.patch, m->kp, act, st));
+  {
+    GemmEpi e;
+    e.bias = static_cast<const float*>(m->w.patch_b);
+    e.pos = static_cast<const float*>(m->w.pos);
+    e.out = w.x[0];
+    e.rows_in = m->n_patches;
+    e.rows_out = s.t[0];
+    e.row_off = 1;
+    TA_TRY(linear(m, w.patches, m->w.patch_w, B * m->n_patches, D, m->kp, EPI_PATCH, e, st));
+  }
+  TA_TRY(insert_rows(w.x[0], B, s.t[0], D, static_cast<const float*>(m->w.cls),
+                     static_cast<const float*>(m->w.pos), ptab, task_ids, 0,
+                     gamma > 0 ? gamma : 0, N, st));
+
+  int cur = 0;
+  const float* size = nullptr;
+  int size_buf = 0;
+  size_t trace_off = 0;
+  int t = s.t[0];
+  for (int l = 0; l < L; ++l) {
+    const ta_layer_weights& Lw = m->layers[l];
+    t = s.t[l];
+    if (l > 0 && gamma > 0)
+      TA_TRY(insert_rows(w.x[cur], B, t, D, nullptr, nullptr, ptab, task_ids, l, gamma,
+                         accumulate ? t - gamma : N, st));
+    const int M = B * t;
+    TA_TRY(layernorm(w.x[cur], static_cast<const float*>(Lw.ln1_w),
+                     static_cast<const float*>(Lw.ln1_b), w.h, M, D, act, st));
+    {
+      GemmEpi e;
+      e.bias = static_cast<const float*>(Lw.qkv_b);
+      e.out = w.qkv;
+      TA_TRY(linear(m, w.h, Lw.qkv_w, M, 3 * D, D, EPI_BIAS, e, st));
+    }
+    TA_TRY(attention(w.qkv, size, B, t, d.heads, m->hd, w.attn, act, st));
+    {
+      GemmEpi e;
+      e.bias = static_cast<const float*>(Lw.proj_b);
+      e.resid = w.x[cur];
+      e.out = w.x[cur];
+      TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID, e, st));
+    }
+    const int r = s.r[l];
+    int tp = t;
+    if (r > 0) {
+      const int na = (t + 1) / 2;
+      int32_t *src = w.src, *dst = w.dst, *unm = w.unm;
+      const int32_t* base = forced_trace ? forced_trace : merge_trace;
+      if (base) {
+        src = const_cast<int32_t*>(base) + trace_off;
+        dst = src + static_cast<size_t>(B) * r;
+        unm = dst + static_cast<size_t>(B) * r;
+      }
+      trace_off += static_cast<size_t>(B) * (2 * r + na - r);
+      if (!forced_trace)
+        TA_TRY(match(nullptr, w.qkv, act, B, t, d.heads, m->hd, r, src, dst, unm, st));
+      else if (merge_trace)
+        cudaMemcpyAsync(merge_trace + (src - forced_trace), src,
+                        sizeof(int32_t) * static_cast<size_t>(B) * (2 * r + na - r),
+                        cudaMemcpyDeviceToDevice, st);
+      TA_TRY(merge(w.x[cur], size, B, t, D, r, src, dst, unm, static_cast<const float*>(Lw.ln2_w),
+                   static_cast<const float*>(Lw.ln2_b), w.x[cur ^ 1], w.size[size_buf], w.h, act,
+                   st));
+      cur ^= 1;
+      size = w.size[size_buf];
+      size_buf ^= 1;
+      tp = t - r;
+    } else {
+      TA_TRY(layernorm(w.x[cur], static_cast<const float*>(Lw.ln2_w),
+                       static_cast<const float*>(Lw.ln2_b), w.h, M, D, act, st));
+    }
+    const int Mp = B * tp;
+    {
+      GemmEpi e;
+      e.bias = static_cast<const float*>(Lw.fc1_b);
+      e.out = w.mlp;
+      TA_TRY(linear(m, w.h, Lw.fc1_w, Mp, d.mlp_dim, D, EPI_BIAS_GELU, e, st));
+    }
+    {
+      GemmEpi e;
+      e.bias = static_cast<const float*>(Lw.fc2_b);
+      e.resid = w.x[cur];
+      if (gamma > 0 && accumulate && l + 1 < L) {
+        // re-stride rows so the next layer's gamma prompt rows follow each image
+        e.out = w.x[cur ^ 1];
+        e.rows_in = tp;
+        e.rows_out = s.t[l + 1];
+        e.row_off = 0;
+        TA_TRY(linear(m, w.mlp, Lw.fc2_w, Mp, D, d.mlp_dim, EPI_BIAS_RESID, e, st));
+        cur ^= 1;
+      } else {
+        e.out = w.x[cur];
+        TA_TRY(linear(m, w.mlp, Lw.fc2_w, Mp, D, d.mlp_dim, EPI_BIAS_RESID, e, st));
+      }
+    }
+    t = tp;
+  }
+  TA_TRY(head(w.x[cur], B, t, D, static_cast<const float*>(m->w.norm_w),
+              static_cast<const float*>(m->w.norm_b), m->heads_dev, task_ids, logits,
+              d.max_classes, st));
+  return TA_OK;
+}
+
+int ta_forward_host(ta_model* m, const float* images_host, const int32_t* task_ids_host, int B,
+                    int gamma, float* logits_host, void* stream) {
+  if (!m || !images_host || !task_ids_host || !logits_host || B <= 0) return TA_ERR_INVALID;
+  for (int i = 0; i < B; ++i)
+    if (task_ids_host[i] < 0 || task_ids_host[i] >= m->d.n_tasks) return TA_ERR_INVALID;
+  if (gamma > 0) {
+    auto it = m->prompts.find(gamma);
+    if (it == m->prompts.end()) return TA_ERR_NO_PROMPT;
+    for (int i = 0; i < B; ++i)
+      if (!it->second[task_ids_host[i]]) return TA_ERR_NO_PROMPT;
+  }
+  std::lock_guard<std::mutex> lock(m->host_mu);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t img_bytes = static_cast<size_t>(B) * 3 * m->d.img * m->d.img * sizeof(float);
+  const size_t task_bytes = align_up(static_cast<size_t>(B) * sizeof(int32_t));
+  const size_t logit_bytes = align_up(static_cast<size_t>(B) * m->d.max_classes * sizeof(float));
+  size_t ws = 0;
+  TA_TRY(ta_workspace_size(m, B, gamma, &ws));
+  const size_t need = align_up(img_bytes) + task_bytes + logit_bytes + ws;
+  if (m->host_ws_bytes < need) {
+    if (m->host_ws) cudaFree(m->host_ws);
+    m->host_ws = nullptr;
+    m->host_ws_bytes = 0;
+    cudaError_t e = cudaMalloc(&m->host_ws, need);
+    if (e != cudaSuccess) return set_last_cuda_error(e);
+    m->host_ws_bytes = need;
+  }
+  char* p = static_cast<char*>(m->host_ws);
+  float* img = reinterpret_cast<float*>(p);
+  int32_t* tasks = reinterpret_cast<int32_t*>(p + align_up(img_bytes));
+  float* logits = reinterpret_cast<float*>(p + align_up(img_bytes) + task_bytes);
+  char* wsp = p + align_up(img_bytes) + task_bytes + logit_bytes;
+  cudaError_t e = cudaMemcpyAsync(img, images_host, img_bytes, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return set_last_cuda_error(e);
+  e = cudaMemcpyAsync(tasks, task_ids_host, B * sizeof(int32_t), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return set_last_cuda_error(e);
+  TA_TRY(ta_forward(m, img, tasks, B, gamma, logits, nullptr, nullptr, wsp, ws, stream));
+  e = cudaMemcpyAsync(logits_host, logits, static_cast<size_t>(B) * m->d.max_classes * sizeof(float),
+                      cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return set_last_cuda_error(e);
+  e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
+// ------------------------------------------------------------------ unit entry points
+int ta_match(const float* metric, int batch, int t, int c, int r, int32_t* src, int32_t* dst,
+             int32_t* unm, void* stream) {
+  if (!metric || !src || !dst || !unm || batch <= 0) return TA_ERR_INVALID;
+  return match(metric, nullptr, TA_DTYPE_F32, batch, t, 1, c, r, src, dst, unm,
+               static_cast<cudaStream_t>(stream));
+}
+
+int ta_merge(const float* x, const float* size, int batch, int t, int dim, int r,
+             const int32_t* src, const int32_t* dst, const int32_t* unm, const float* ln_w,
+             const float* ln_b, float* x_out, float* size_out, void* h_out, int h_dtype,
+             void* stream) {
+  if (!x || !src || !dst || !unm || !ln_w || !ln_b || !x_out || !size_out || !h_out || batch <= 0)
+    return TA_ERR_INVALID;
+  return merge(x, size, batch, t, dim, r, src, dst, unm, ln_w, ln_b, x_out, size_out, h_out,
+               h_dtype, static_cast<cudaStream_t>(stream));
+}
+
+int ta_attention(const void* qkv, const float* size, int batch, int t, int heads, int head_dim,
+                 void* out, int dtype, void* stream) {
+  if (!qkv || !out || batch <= 0 || heads <= 0) return TA_ERR_INVALID;
+  return attention(qkv, size, batch, t, heads, head_dim, out, dtype,
+                   static_cast<cudaStream_t>(stream));
+}
+
+int ta_gemm(const void* a, const void* w, const float* bias, const float* resid, void* out, int m,
+            int n, int k, int epilogue, int dtype, int out_dtype, void* stream) {
+  if (!a || !w || !bias || !out || epilogue < 0 || epilogue > 2) return TA_ERR_INVALID;
+  if (epilogue == EPI_BIAS_RESID && (!resid || out_dtype != TA_DTYPE_F32)) return TA_ERR_INVALID;
+  GemmEpi e;
+  e.bias = bias;
+  e.resid = resid;
+  e.out = out;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == TA_DTYPE_BF16) return gemm_bf16(a, w, m, n, k, epilogue, out_dtype == TA_DTYPE_BF16, e, st);
+  if (out_dtype != TA_DTYPE_F32) return TA_ERR_INVALID;
+  return gemm_f32(static_cast<const float*>(a), static_cast<const float*>(w), m, n, k, epilogue, e, st);
+}
+
+int ta_layernorm(const float* x, const float* w, const float* b, void* out, int rows, int dim,
+                 int out_dtype, void* stream) {
+  if (!x || !w || !b || !out) return TA_ERR_INVALID;
+  return layernorm(x, w, b, out, rows, dim, out_dtype, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

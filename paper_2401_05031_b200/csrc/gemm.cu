@@ -1,0 +1,425 @@
+// Linear layers of the token-adapted ViT:
+//   C[m, n] = sum_k A[m, k] * W[n, k]  + fused epilogue (bias / GELU / residual / pos).
+//
+// bf16 path: persistent, warp-specialised tcgen05 kernel.
+//   warp 0      TMA producer (one elected lane): A and W tiles -> SW128 smem ring
+//   warp 1      MMA issuer (one lane): tcgen05.mma kind::f16 128 x BN x 16 into TMEM
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue: tcgen05.ld -> registers -> bias/GELU/residual -> HBM
+// Two TMEM accumulator stages let the epilogue of tile i overlap the MMAs of tile i+1.
+// The token count per layer varies with gamma, so M is a runtime value; rows past M are
+// zero-filled by TMA and masked in the epilogue.
+//
+// fp32 path: SIMT FFMA tile kernel with the same epilogues, used by the fp32 parity
+// mode (north_star: merge index sets bit-exact in fp32 mode).
+#include <cstdio>
+#include <mutex>
+
+#include <cudaTypedefs.h>
+
+#include "common.h"
+#include "ptx.cuh"
+
+namespace ta {
+
+// ------------------------------------------------------------------ epilogue
+template <int EPI, typename OutT>
+__device__ __forceinline__ void epi_store32(const GemmEpi& e, int N, long long m, int n0,
+                                            float (&v)[32]) {
+  const long long orow = epi_out_row(e, m);
+  const float4* b4 = reinterpret_cast<const float4*>(e.bias + n0);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 b = __ldg(b4 + j);
+    v[4 * j + 0] += b.x;
+    v[4 * j + 1] += b.y;
+    v[4 * j + 2] += b.z;
+    v[4 * j + 3] += b.w;
+  }
+  if constexpr (EPI == EPI_BIAS_GELU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+  }
+  if constexpr (EPI == EPI_BIAS_RESID) {
+    const float4* r4 = reinterpret_cast<const float4*>(e.resid + m * N + n0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float4 r = r4[j];
+      v[4 * j + 0] += r.x;
+      v[4 * j + 1] += r.y;
+      v[4 * j + 2] += r.z;
+      v[4 * j + 3] += r.w;
+    }
+  }
+  if constexpr (EPI == EPI_PATCH) {
+    const long long prow = e.row_off + (m % e.rows_in);
+    const float4* p4 = reinterpret_cast<const float4*>(e.pos + prow * N + n0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float4 p = __ldg(p4 + j);
+      v[4 * j + 0] += p.x;
+      v[4 * j + 1] += p.y;
+      v[4 * j + 2] += p.z;
+      v[4 * j + 3] += p.w;
+    }
+  }
+  if constexpr (sizeof(OutT) == 2) {
+    uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(e.out) + orow * N + n0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint4 w;
+      w.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
+      w.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
+      w.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
+      w.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
+      o[j] = w;
+    }
+  } else {
+    float4* o = reinterpret_cast<float4*>(static_cast<float*>(e.out) + orow * N + n0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      o[j] = make_float4(v[4 * j + 0], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  }
+}
+
+// ------------------------------------------------------------------ tcgen05 kernel
+constexpr int kBM = 128;
+constexpr int kBK = 64;  // 64 bf16 = 128 B rows -> SWIZZLE_128B
+constexpr int kGemmThreads = 256;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;  // two accumulator stages
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN, int EPI, typename OutT>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_bf16_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
+                           const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                           GemmEpi epi) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // Inputs (A) may be produced by the previous kernel in the stream (PDL).
+  grid_dep_wait();
+
+  const int num_m = (M + kBM - 1) / kBM;
+  const int num_n = N / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = K / kBK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_blk = tile / num_n;
+        const int n_blk = tile - m_blk * num_n;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * Cfg::kStageBytes;
+          uint8_t* sb = sa + Cfg::kABytes;
+          mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+          tma_load_2d(&tmA, &full[stage], sa, kb * kBK, m_blk * kBM);
+          tma_load_2d(&tmB, &full[stage], sb, kb * kBK, n_blk * BN);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(kBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * Cfg::kStageBytes);
+          const uint32_t sb = sa + Cfg::kABytes;
+          const uint64_t adesc = umma_desc_sw128(sa);
+          const uint64_t bdesc = umma_desc_sw128(sb);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            // +32 bytes per K=16 step inside the 128-byte swizzle row (encoded >> 4).
+            umma_f16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t ew = warp - 4;  // == warp % 4: TMEM lanes [32*ew, 32*ew + 32)
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int m_blk = tile / num_n;
+      const int n_blk = tile - m_blk * num_n;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const long long m = static_cast<long long>(m_blk) * kBM + ew * 32 + lane;
+      const uint32_t t_row = tmem_base + ((ew * 32u) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_row + c * 32, r);
+        tmem_ld_wait();
+        if (c == BN / 32 - 1) {
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+        }
+        if (m < M) {
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          epi_store32<EPI, OutT>(epi, N, m, n_blk * BN + c * 32, v);
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  grid_dep_launch();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<GemmCfg<BN>::kTmemCols>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ SIMT fp32 kernel
+// 128 x 128 tile, BK = 8, 256 threads, 8 x 8 outputs per thread.  fp32 FFMA only:
+// products are exact fp32 so results differ from a CPU fp32 GEMM by summation order.
+template <int EPI>
+__global__ void __launch_bounds__(256) gemm_f32_simt_kernel(const float* __restrict__ A,
+                                                            const float* __restrict__ W, int M,
+                                                            int N, int K, GemmEpi epi) {
+  __shared__ float As[2][8][128 + 4];
+  __shared__ float Bs[2][8][128 + 4];
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.y * 128;
+  const int n0 = blockIdx.x * 128;
+  const int tr = tid / 16;  // 16 x 16 thread grid
+  const int tc = tid % 16;
+  float acc[8][8] = {};
+  // Loader: 128 rows x 8 k per operand = 1024 floats = 256 threads x 4 (one float4).
+  const int lrow = tid / 2;
+  const int lk = (tid % 2) * 4;
+  auto load = [&](int buf, int k0) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (m0 + lrow < M) a = *reinterpret_cast<const float4*>(A + (long long)(m0 + lrow) * K + k0 + lk);
+    const float4 b = *reinterpret_cast<const float4*>(W + (long long)(n0 + lrow) * K + k0 + lk);
+    As[buf][lk + 0][lrow] = a.x;
+    As[buf][lk + 1][lrow] = a.y;
+    As[buf][lk + 2][lrow] = a.z;
+    As[buf][lk + 3][lrow] = a.w;
+    Bs[buf][lk + 0][lrow] = b.x;
+    Bs[buf][lk + 1][lrow] = b.y;
+    Bs[buf][lk + 2][lrow] = b.z;
+    Bs[buf][lk + 3][lrow] = b.w;
+  };
+  load(0, 0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < K; k0 += 8) {
+    if (k0 + 8 < K) load(buf ^ 1, k0 + 8);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      float a[8], b[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = As[buf][kk][tr * 4 + i];
+        a[4 + i] = As[buf][kk][64 + tr * 4 + i];
+        b[i] = Bs[buf][kk][tc * 4 + i];
+        b[4 + i] = Bs[buf][kk][64 + tc * 4 + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const long long m = m0 + (i < 4 ? tr * 4 + i : 64 + tr * 4 + (i - 4));
+    if (m >= M) continue;
+    const long long orow = epi_out_row(epi, m);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int n = n0 + (j < 4 ? tc * 4 + j : 64 + tc * 4 + (j - 4));
+      float v = acc[i][j] + epi.bias[n];
+      if (EPI == EPI_BIAS_GELU) v = gelu_erf(v);
+      if (EPI == EPI_BIAS_RESID) v = epi.resid[m * N + n] + v;
+      if (EPI == EPI_PATCH) v += epi.pos[(epi.row_off + m % epi.rows_in) * (long long)N + n];
+      static_cast<float*>(epi.out)[orow * N + n] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// Row-major bf16 matrix [rows, cols] as a 2D tensor map with a (64 x box_rows) SW128 box.
+int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                      uint32_t box_rows) {
+  auto enc = get_encode_fn();
+  if (!enc) return TA_ERR_CUDA;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? TA_OK : TA_ERR_SHAPE;
+}
+
+template <int BN, int EPI, typename OutT>
+static int launch_bf16(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, int N, int K,
+                       const GemmEpi& epi, cudaStream_t stream) {
+  using Cfg = GemmCfg<BN>;
+  auto kern = gemm_bf16_sm100_kernel<BN, EPI, OutT>;
+  static bool attr_set = false;  // per instantiation; benign race (idempotent)
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::kSmemBytes);
+    if (e != cudaSuccess) return set_last_cuda_error(e);
+    attr_set = true;
+  }
+  const int tiles = ((M + kBM - 1) / kBM) * (N / BN);
+  const int grid = tiles < device_sm_count() ? tiles : device_sm_count();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta_, tb_, M, N, K, epi);
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
+template <int BN>
+static int dispatch_bf16(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
+                         int epi_kind, bool out_bf16, const GemmEpi& epi, cudaStream_t s) {
+  switch (epi_kind) {
+    case EPI_BIAS:
+      return out_bf16 ? launch_bf16<BN, EPI_BIAS, __nv_bfloat16>(a, b, M, N, K, epi, s)
+                      : launch_bf16<BN, EPI_BIAS, float>(a, b, M, N, K, epi, s);
+    case EPI_BIAS_GELU:
+      return out_bf16 ? launch_bf16<BN, EPI_BIAS_GELU, __nv_bfloat16>(a, b, M, N, K, epi, s)
+                      : launch_bf16<BN, EPI_BIAS_GELU, float>(a, b, M, N, K, epi, s);
+    case EPI_BIAS_RESID:
+      return launch_bf16<BN, EPI_BIAS_RESID, float>(a, b, M, N, K, epi, s);
+    case EPI_PATCH:
+      return launch_bf16<BN, EPI_PATCH, float>(a, b, M, N, K, epi, s);
+  }
+  return TA_ERR_INVALID;
+}
+
+int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, bool out_bf16,
+              const GemmEpi& epi, cudaStream_t stream) {
+  if (M <= 0) return TA_OK;
+  if (K % kBK != 0 || N % 128 != 0) return TA_ERR_SHAPE;
+  if ((epi_kind == EPI_BIAS_RESID || epi_kind == EPI_PATCH) && out_bf16) return TA_ERR_INVALID;
+  const int BN = (N % 256 == 0) ? 256 : 128;
+  CUtensorMap ta_, tb_;
+  int rc = make_tmap_bf16_2d(&ta_, A, M, K, kBM);
+  if (rc) return rc;
+  rc = make_tmap_bf16_2d(&tb_, W, N, K, BN);
+  if (rc) return rc;
+  return BN == 256 ? dispatch_bf16<256>(ta_, tb_, M, N, K, epi_kind, out_bf16, epi, stream)
+                   : dispatch_bf16<128>(ta_, tb_, M, N, K, epi_kind, out_bf16, epi, stream);
+}
+
+int gemm_f32(const float* A, const float* W, int M, int N, int K, int epi_kind,
+             const GemmEpi& epi, cudaStream_t stream) {
+  if (M <= 0) return TA_OK;
+  if (K % 8 != 0 || N % 128 != 0) return TA_ERR_SHAPE;
+  dim3 grid(N / 128, (M + 127) / 128);
+  switch (epi_kind) {
+    case EPI_BIAS: gemm_f32_simt_kernel<EPI_BIAS><<<grid, 256, 0, stream>>>(A, W, M, N, K, epi); break;
+    case EPI_BIAS_GELU: gemm_f32_simt_kernel<EPI_BIAS_GELU><<<grid, 256, 0, stream>>>(A, W, M, N, K, epi); break;
+    case EPI_BIAS_RESID: gemm_f32_simt_kernel<EPI_BIAS_RESID><<<grid, 256, 0, stream>>>(A, W, M, N, K, epi); break;
+    case EPI_PATCH: gemm_f32_simt_kernel<EPI_PATCH><<<grid, 256, 0, stream>>>(A, W, M, N, K, epi); break;
+    default: return TA_ERR_INVALID;
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
+}  // namespace ta

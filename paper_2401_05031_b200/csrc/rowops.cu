@@ -1,0 +1,225 @@
+// Row-wise bandwidth kernels of the forward:
+//   patchify     images fp32 NCHW -> patch matrix [B*Np, Kp] (im2col for the P x P / stride P conv)
+//   insert_rows  cls row (layer 0) and per-task prompt rows P[task][gamma][l] (VPT prompt module)
+//   layernorm    fp32 rows -> act dtype (timm eps 1e-6)
+//   head         final LayerNorm on the cls row + per-task linear head (TaskModel head)
+// All are HBM-bound: one warp per row, 16-byte vector accesses, fp32 statistics.
+#include "common.h"
+#include "ptx.cuh"
+
+namespace ta {
+
+// ------------------------------------------------------------------ patchify
+// out[b*Np + py*G + px, c*P*P + ky*P + kx] = img[b, c, py*P + ky, px*P + kx]; cols >= 3P^2 zero.
+template <typename T>
+__global__ void patchify_kernel(const float* __restrict__ img, T* __restrict__ out, int B, int S,
+                                int P, int Kp) {
+  const int G = S / P;
+  const int Np = G * G;
+  const int K = 3 * P * P;
+  const long long total = static_cast<long long>(B) * Np * Kp;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int col = static_cast<int>(i % Kp);
+    const long long row = i / Kp;
+    float v = 0.f;
+    if (col < K) {
+      const int b = static_cast<int>(row / Np);
+      const int p = static_cast<int>(row % Np);
+      const int py = p / G, px = p % G;
+      const int c = col / (P * P);
+      const int rem = col % (P * P);
+      const int ky = rem / P, kx = rem % P;
+      v = img[((static_cast<long long>(b) * 3 + c) * S + py * P + ky) * S + px * P + kx];
+    }
+    if constexpr (sizeof(T) == 2)
+      out[i] = __float2bfloat16_rn(v);
+    else
+      out[i] = v;
+  }
+}
+
+int patchify(const float* img, void* out, int B, int S, int P, int Kp, int dtype,
+             cudaStream_t s) {
+  const long long total = static_cast<long long>(B) * (S / P) * (S / P) * Kp;
+  const int grid = static_cast<int>((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+  if (dtype == TA_DTYPE_BF16)
+    patchify_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(img, static_cast<__nv_bfloat16*>(out), B, S, P, Kp);
+  else
+    patchify_kernel<float><<<grid, 256, 0, s>>>(img, static_cast<float*>(out), B, S, P, Kp);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
+// ------------------------------------------------------------------ insert rows
+// x is [B, t_total, D] fp32.  If cls != null: row 0 = cls + pos[0].  If gamma > 0: rows
+// [prompt_row, prompt_row + gamma) = prompts[task_b][layer] (a [gamma, D] block found via
+// the per-task pointer table; prompts are fp32 [depth, gamma, D]).
+__global__ void insert_rows_kernel(float* __restrict__ x, int t_total, int D,
+                                   const float* __restrict__ cls, const float* __restrict__ pos,
+                                   const float* const* __restrict__ prompt_tab,
+                                   const int32_t* __restrict__ task_ids, int layer, int gamma,
+                                   int prompt_row) {
+  const int b = blockIdx.x;
+  float* xb = x + static_cast<long long>(b) * t_total * D;
+  if (cls != nullptr) {
+    for (int c = threadIdx.x; c < D; c += blockDim.x) xb[c] = cls[c] + pos[c];
+  }
+  if (gamma > 0) {
+    const float* P = prompt_tab[task_ids[b]] + static_cast<long long>(layer) * gamma * D;
+    float4* dst = reinterpret_cast<float4*>(xb + static_cast<long long>(prompt_row) * D);
+    const float4* src = reinterpret_cast<const float4*>(P);
+    for (int i = threadIdx.x; i < gamma * D / 4; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
+int insert_rows(float* x, int B, int t_total, int D, const float* cls, const float* pos,
+                const float* const* prompt_tab, const int32_t* task_ids, int layer, int gamma,
+                int prompt_row, cudaStream_t s) {
+  insert_rows_kernel<<<B, 256, 0, s>>>(x, t_total, D, cls, pos, prompt_tab, task_ids, layer,
+                                       gamma, prompt_row);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
+// ------------------------------------------------------------------ layernorm
+// One warp per row; VEC float4 per lane (D = 128 * VEC).  Two-pass mean / variance in
+// registers (biased variance, as torch.nn.LayerNorm).
+template <int VEC, typename T>
+__global__ void layernorm_kernel(const float* __restrict__ x, const float* __restrict__ w,
+                                 const float* __restrict__ bvec, T* __restrict__ out, int rows) {
+  constexpr int D = 128 * VEC;
+  grid_dep_wait();
+  const int row = blockIdx.x * (blockDim.x / 32) + warp_id();
+  if (row < rows) {
+    const int lane = lane_id();
+    const float4* xr = reinterpret_cast<const float4*>(x + static_cast<long long>(row) * D);
+    float4 v[VEC];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      v[i] = xr[lane + 32 * i];
+      s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    }
+    const float mean = warp_sum(s) / D;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, d = v[i].w - mean;
+      q += (a * a + b * b) + (c * c + d * d);
+    }
+    const float rstd = 1.0f / sqrtf(warp_sum(q) / D + 1e-6f);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      const int c = 4 * (lane + 32 * i);
+      const float4 g = __ldg(reinterpret_cast<const float4*>(w) + lane + 32 * i);
+      const float4 bb = __ldg(reinterpret_cast<const float4*>(bvec) + lane + 32 * i);
+      const float y0 = (v[i].x - mean) * rstd * g.x + bb.x;
+      const float y1 = (v[i].y - mean) * rstd * g.y + bb.y;
+      const float y2 = (v[i].z - mean) * rstd * g.z + bb.z;
+      const float y3 = (v[i].w - mean) * rstd * g.w + bb.w;
+      if constexpr (sizeof(T) == 2) {
+        uint2 p;
+        p.x = pack_bf16(y0, y1);
+        p.y = pack_bf16(y2, y3);
+        *reinterpret_cast<uint2*>(out + static_cast<long long>(row) * D + c) = p;
+      } else {
+        *reinterpret_cast<float4*>(out + static_cast<long long>(row) * D + c) =
+            make_float4(y0, y1, y2, y3);
+      }
+    }
+  }
+  grid_dep_launch();
+}
+
+template <typename T>
+static int ln_dispatch(const float* x, const float* w, const float* b, T* out, int rows, int D,
+                       cudaStream_t s) {
+  const int grid = (rows + 7) / 8;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  switch (D) {
+    case 256: e = cudaLaunchKernelEx(&cfg, layernorm_kernel<2, T>, x, w, b, out, rows); break;
+    case 768: e = cudaLaunchKernelEx(&cfg, layernorm_kernel<6, T>, x, w, b, out, rows); break;
+    case 1024: e = cudaLaunchKernelEx(&cfg, layernorm_kernel<8, T>, x, w, b, out, rows); break;
+    case 1280: e = cudaLaunchKernelEx(&cfg, layernorm_kernel<10, T>, x, w, b, out, rows); break;
+    default: return TA_ERR_SHAPE;
+  }
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
+int layernorm(const float* x, const float* w, const float* b, void* out, int rows, int D,
+              int out_dtype, cudaStream_t s) {
+  if (rows <= 0) return TA_OK;
+  if (out_dtype == TA_DTYPE_BF16)
+    return ln_dispatch(x, w, b, static_cast<__nv_bfloat16*>(out), rows, D, s);
+  return ln_dispatch(x, w, b, static_cast<float*>(out), rows, D, s);
+}
+
+// ------------------------------------------------------------------ head
+// logits[b, c] = LN(x[b, 0, :]) . W_task[c] + b_task[c] for c < C_task, -inf beyond.
+__global__ void head_kernel(const float* __restrict__ x, int t_total, int D,
+                            const float* __restrict__ nw, const float* __restrict__ nb,
+                            const HeadDesc* __restrict__ heads, const int32_t* __restrict__ task,
+                            float* __restrict__ logits, int c_max) {
+  extern __shared__ float hrow[];
+  __shared__ float red[32];
+  const int b = blockIdx.x;
+  const float* xr = x + static_cast<long long>(b) * t_total * D;
+  const int nwarps = blockDim.x / 32;
+  float s = 0.f;
+  for (int c = threadIdx.x; c < D; c += blockDim.x) {
+    hrow[c] = xr[c];
+    s += hrow[c];
+  }
+  s = warp_sum(s);
+  if (lane_id() == 0) red[warp_id()] = s;
+  __syncthreads();
+  float tot = 0.f;
+  for (int i = 0; i < nwarps; ++i) tot += red[i];
+  const float mean = tot / D;
+  __syncthreads();
+  float q = 0.f;
+  for (int c = threadIdx.x; c < D; c += blockDim.x) {
+    const float d = hrow[c] - mean;
+    q += d * d;
+  }
+  q = warp_sum(q);
+  if (lane_id() == 0) red[warp_id()] = q;
+  __syncthreads();
+  float qt = 0.f;
+  for (int i = 0; i < nwarps; ++i) qt += red[i];
+  const float rstd = 1.0f / sqrtf(qt / D + 1e-6f);
+  for (int c = threadIdx.x; c < D; c += blockDim.x) hrow[c] = (hrow[c] - mean) * rstd * nw[c] + nb[c];
+  __syncthreads();
+  const HeadDesc h = heads[task[b]];
+  for (int c = warp_id(); c < c_max; c += nwarps) {
+    float acc = 0.f;
+    if (c < h.classes) {
+      const float* wr = h.w + static_cast<long long>(c) * D;
+      for (int k = lane_id(); k < D; k += 32) acc += hrow[k] * wr[k];
+      acc = warp_sum(acc);
+      acc += h.b[c];
+    } else {
+      acc = -INFINITY;
+    }
+    if (lane_id() == 0) logits[static_cast<long long>(b) * c_max + c] = acc;
+  }
+}
+
+int head(const float* x, int B, int t_total, int D, const float* nw, const float* nb,
+         const HeadDesc* heads, const int32_t* task, float* logits, int c_max, cudaStream_t s) {
+  head_kernel<<<B, 256, D * sizeof(float), s>>>(x, t_total, D, nw, nb, heads, task, logits, c_max);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
+}  // namespace ta

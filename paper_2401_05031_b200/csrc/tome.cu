@@ -1,0 +1,317 @@
+// Token merging (Appendix A `match` / `merge`):
+//   match  ToMe bipartite soft matching: metric = mean_h k (optional), L2 normalise,
+//          S = A B^T over alternating token sets (A = even rows incl. cls, B = odd rows),
+//          S[cls, :] = -inf, row max/argmax (ties -> lowest column), top-r rows by a
+//          stable descending order (rank counting: exact and deterministic),
+//          unm = the remaining A rows ascending.
+//   merge  size-weighted average: B_j <- (s_j x_j + sum_{i: dst_i = j} s_i x_i) / (s_j + sum s_i),
+//          output order [A unmerged (cls first); B all], fused LayerNorm (LN2) of the
+//          merged rows in the activation dtype.
+// The per-image problem is small (A 99 x B 98 x 64 at t = 197) and latency-bound, so one
+// CTA owns one image; the merge is HBM-bound (read t x D, write t' x D fp32 + t' x D act).
+#include <cfloat>
+
+#include "common.h"
+#include "ptx.cuh"
+
+namespace ta {
+
+constexpr int kMatchThreads = 256;
+
+// Dynamic smem: A rows [na][c+1], B rows [nb][c+1] (fp32, padded), node_max [na],
+// node_idx [na], rank [na].
+template <typename QT>
+__global__ void __launch_bounds__(kMatchThreads)
+    match_kernel(const float* __restrict__ metric, const QT* __restrict__ qkv, int t, int heads,
+                 int c, int r, int32_t* __restrict__ src_out, int32_t* __restrict__ dst_out,
+                 int32_t* __restrict__ unm_out) {
+  extern __shared__ float sm[];
+  const int b = blockIdx.x;
+  const int na = (t + 1) / 2;
+  const int nb = t / 2;
+  const int cs = c + 1;
+  float* As = sm;
+  float* Bs = As + na * cs;
+  float* node_max = Bs + nb * cs;
+  int* node_idx = reinterpret_cast<int*>(node_max + na);
+  int* rank = node_idx + na;
+  const int warp = warp_id(), lane = lane_id(), nwarps = blockDim.x / 32;
+
+  grid_dep_wait();
+  // 1) metric rows (mean over heads, fixed head order), then L2-normalise (x / ||x||).
+  for (int row = warp; row < t; row += nwarps) {
+    float* dstrow = (row & 1) ? Bs + (row >> 1) * cs : As + (row >> 1) * cs;
+    float ss = 0.f;
+    for (int j = lane; j < c; j += 32) {
+      float v;
+      if (metric != nullptr) {
+        v = metric[(static_cast<long long>(b) * t + row) * c + j];
+      } else {
+        const long long D = static_cast<long long>(heads) * c;
+        const QT* kr = qkv + (static_cast<long long>(b) * t + row) * 3 * D + D + j;
+        float acc = 0.f;
+        for (int h = 0; h < heads; ++h) acc += static_cast<float>(kr[h * c]);
+        v = acc / heads;
+      }
+      dstrow[j] = v;
+      ss += v * v;
+    }
+    const float nrm = sqrtf(warp_sum(ss));
+    for (int j = lane; j < c; j += 32) dstrow[j] = dstrow[j] / nrm;
+  }
+  __syncthreads();
+
+  // 2) scores and row max / argmax (lowest column on ties); row 0 (cls) is -inf.
+  for (int i = warp; i < na; i += nwarps) {
+    float best = -INFINITY;
+    int best_j = 0;
+    if (i > 0) {
+      const float* ar = As + i * cs;
+      for (int j = lane; j < nb; j += 32) {
+        const float* br = Bs + j * cs;
+        float acc = 0.f;
+        for (int k = 0; k < c; ++k) acc = fmaf(ar[k], br[k], acc);
+        if (acc > best) {  // j increases per lane: strict > keeps the lowest j
+          best = acc;
+          best_j = j;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, best_j, o);
+        if (ov > best || (ov == best && oj < best_j)) {
+          best = ov;
+          best_j = oj;
+        }
+      }
+    }
+    if (lane == 0) {
+      node_max[i] = best;
+      node_idx[i] = best_j;
+    }
+  }
+  __syncthreads();
+
+  // 3) rank in the stable descending order: rank_i = #{j : v_j > v_i or (v_j == v_i and j < i)}.
+  for (int i = threadIdx.x; i < na; i += blockDim.x) {
+    const float vi = node_max[i];
+    int rk = 0;
+    for (int j = 0; j < na; ++j) {
+      const float vj = node_max[j];
+      rk += (vj > vi) || (vj == vi && j < i);
+    }
+    rank[i] = rk;
+  }
+  __syncthreads();
+
+  // 4) src/dst by rank; unm = rows with rank >= r in ascending index order.
+  int32_t* srcb = src_out + static_cast<long long>(b) * r;
+  int32_t* dstb = dst_out + static_cast<long long>(b) * r;
+  int32_t* unmb = unm_out + static_cast<long long>(b) * (na - r);
+  for (int i = threadIdx.x; i < na; i += blockDim.x) {
+    const int rk = rank[i];
+    if (rk < r) {
+      srcb[rk] = i;
+      dstb[rk] = node_idx[i];
+    } else {
+      int pos = 0;
+      for (int j = 0; j < i; ++j) pos += rank[j] >= r;
+      unmb[pos] = i;
+    }
+  }
+  grid_dep_launch();
+}
+
+int match(const float* metric, const void* qkv, int qkv_dtype, int B, int t, int heads, int c,
+          int r, int32_t* src, int32_t* dst, int32_t* unm, cudaStream_t s) {
+  const int na = (t + 1) / 2, nb = t / 2;
+  if (r <= 0 || r > na - 1 || t < 3) return TA_ERR_INVALID;
+  const size_t smem = (static_cast<size_t>(na + nb) * (c + 1) + 3 * na) * sizeof(float);
+  if (smem > 220 * 1024) return TA_ERR_SHAPE;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(B);
+  cfg.blockDim = dim3(kMatchThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (metric != nullptr || qkv_dtype == TA_DTYPE_F32) {
+    auto k = match_kernel<float>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    e = cudaLaunchKernelEx(&cfg, k, metric, static_cast<const float*>(qkv), t, heads, c, r, src,
+                           dst, unm);
+  } else {
+    auto k = match_kernel<__nv_bfloat16>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    e = cudaLaunchKernelEx(&cfg, k, metric, static_cast<const __nv_bfloat16*>(qkv), t, heads, c,
+                           r, src, dst, unm);
+  }
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
+// ------------------------------------------------------------------ merge + LN2
+// grid (B, ceil(t'/ROWS)); one warp per output row; VEC float4 per lane (D = 128 VEC).
+template <int VEC, typename T>
+__global__ void __launch_bounds__(256)
+    merge_kernel(const float* __restrict__ x, const float* __restrict__ size, int t, int r,
+                 const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                 const int32_t* __restrict__ unm, const float* __restrict__ ln_w,
+                 const float* __restrict__ ln_b, float* __restrict__ x_out,
+                 float* __restrict__ size_out, T* __restrict__ h_out) {
+  constexpr int D = 128 * VEC;
+  __shared__ int s_src[256];
+  __shared__ int s_dst[256];
+  const int b = blockIdx.x;
+  const int na = (t + 1) / 2;
+  const int n_unm = na - r;
+  const int tp = t - r;
+  grid_dep_wait();
+  for (int i = threadIdx.x; i < r; i += blockDim.x) {
+    s_src[i] = src[static_cast<long long>(b) * r + i];
+    s_dst[i] = dst[static_cast<long long>(b) * r + i];
+  }
+  __syncthreads();
+  const int lane = lane_id();
+  const float* xb = x + static_cast<long long>(b) * t * D;
+  const float* sb = size != nullptr ? size + static_cast<long long>(b) * t : nullptr;
+  const int rows_per_cta = (blockDim.x / 32) * 4;
+  const int o_begin = blockIdx.y * rows_per_cta;
+  const int o_end = min(tp, o_begin + rows_per_cta);
+  for (int o = o_begin + warp_id(); o < o_end; o += blockDim.x / 32) {
+    float4 acc[VEC];
+    float stot;
+    if (o < n_unm) {
+      const int tok = 2 * unm[static_cast<long long>(b) * n_unm + o];
+      const float s = sb ? sb[tok] : 1.0f;
+      const float4* xr = reinterpret_cast<const float4*>(xb + static_cast<long long>(tok) * D);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        const float4 v = xr[lane + 32 * i];
+        acc[i] = make_float4(v.x * s, v.y * s, v.z * s, v.w * s);
+      }
+      stot = s;
+    } else {
+      const int j = o - n_unm;
+      const int tok = 2 * j + 1;
+      const float s = sb ? sb[tok] : 1.0f;
+      const float4* xr = reinterpret_cast<const float4*>(xb + static_cast<long long>(tok) * D);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        const float4 v = xr[lane + 32 * i];
+        acc[i] = make_float4(v.x * s, v.y * s, v.z * s, v.w * s);
+      }
+      stot = s;
+      // scatter_reduce(sum, include_self) order: self, then sources in src order.
+      for (int q = 0; q < r; ++q) {
+        if (s_dst[q] != j) continue;
+        const int stok = 2 * s_src[q];
+        const float ss = sb ? sb[stok] : 1.0f;
+        const float4* sr = reinterpret_cast<const float4*>(xb + static_cast<long long>(stok) * D);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+          const float4 v = sr[lane + 32 * i];
+          acc[i].x += v.x * ss;
+          acc[i].y += v.y * ss;
+          acc[i].z += v.z * ss;
+          acc[i].w += v.w * ss;
+        }
+        stot += ss;
+      }
+    }
+    // x = (sum s x) / (sum s)
+    float sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      acc[i].x /= stot;
+      acc[i].y /= stot;
+      acc[i].z /= stot;
+      acc[i].w /= stot;
+      sum += (acc[i].x + acc[i].y) + (acc[i].z + acc[i].w);
+    }
+    const long long orow = static_cast<long long>(b) * tp + o;
+    float4* xo = reinterpret_cast<float4*>(x_out + orow * D);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) xo[lane + 32 * i] = acc[i];
+    if (lane == 0) size_out[orow] = stot;
+    // fused LN2
+    const float mean = warp_sum(sum) / D;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      const float a0 = acc[i].x - mean, a1 = acc[i].y - mean, a2 = acc[i].z - mean,
+                  a3 = acc[i].w - mean;
+      q += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
+    }
+    const float rstd = 1.0f / sqrtf(warp_sum(q) / D + 1e-6f);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      const int cidx = 4 * (lane + 32 * i);
+      const float4 g = __ldg(reinterpret_cast<const float4*>(ln_w) + lane + 32 * i);
+      const float4 bb = __ldg(reinterpret_cast<const float4*>(ln_b) + lane + 32 * i);
+      const float y0 = (acc[i].x - mean) * rstd * g.x + bb.x;
+      const float y1 = (acc[i].y - mean) * rstd * g.y + bb.y;
+      const float y2 = (acc[i].z - mean) * rstd * g.z + bb.z;
+      const float y3 = (acc[i].w - mean) * rstd * g.w + bb.w;
+      if constexpr (sizeof(T) == 2) {
+        uint2 p;
+        p.x = pack_bf16(y0, y1);
+        p.y = pack_bf16(y2, y3);
+        *reinterpret_cast<uint2*>(h_out + orow * D + cidx) = p;
+      } else {
+        *reinterpret_cast<float4*>(h_out + orow * D + cidx) = make_float4(y0, y1, y2, y3);
+      }
+    }
+  }
+  grid_dep_launch();
+}
+
+template <typename T>
+static int merge_dispatch(const float* x, const float* size, int B, int t, int D, int r,
+                          const int32_t* src, const int32_t* dst, const int32_t* unm,
+                          const float* ln_w, const float* ln_b, float* x_out, float* size_out,
+                          T* h_out, cudaStream_t s) {
+  const int tp = t - r;
+  const int rows_per_cta = 8 * 4;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(B, (tp + rows_per_cta - 1) / rows_per_cta);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+#define TA_MERGE_CASE(DIM, V)                                                                  \
+  case DIM:                                                                                    \
+    e = cudaLaunchKernelEx(&cfg, merge_kernel<V, T>, x, size, t, r, src, dst, unm, ln_w, ln_b, \
+                           x_out, size_out, h_out);                                            \
+    break;
+  switch (D) {
+    TA_MERGE_CASE(256, 2)
+    TA_MERGE_CASE(768, 6)
+    TA_MERGE_CASE(1024, 8)
+    TA_MERGE_CASE(1280, 10)
+    default: return TA_ERR_SHAPE;
+  }
+#undef TA_MERGE_CASE
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
+int merge(const float* x, const float* size, int B, int t, int D, int r, const int32_t* src,
+          const int32_t* dst, const int32_t* unm, const float* ln_w, const float* ln_b,
+          float* x_out, float* size_out, void* h_out, int h_dtype, cudaStream_t s) {
+  if (r <= 0 || r > (t + 1) / 2 - 1 || r > 256) return TA_ERR_INVALID;
+  if (h_dtype == TA_DTYPE_BF16)
+    return merge_dispatch(x, size, B, t, D, r, src, dst, unm, ln_w, ln_b, x_out, size_out,
+                          static_cast<__nv_bfloat16*>(h_out), s);
+  return merge_dispatch(x, size, B, t, D, r, src, dst, unm, ln_w, ln_b, x_out, size_out,
+                        static_cast<float*>(h_out), s);
+}
+
+}  // namespace ta

@@ -1,0 +1,313 @@
+"""ServeModel / TaskModel / TransformerModel — the paper's serving entry points
+ on the B200 path.
+
+* ``TransformerModel``: the shared ViT backbone with a prompt module before
+  the norm and a merge module before the MLP in every layer; weights live on the GPU in
+  the layouts of include/tokadapt_cuda.h.
+* ``TaskModel``: per-task parameters = prompt tokens per gamma + head.
+* ``ServeModel``: ``forward(inputs, tasks, task_params, gamma)`` over a
+  mixed-task batch at one gamma; ``execute(batch, gamma, payloads)`` is the call an
+  engine makes in place of ``estimate_batch`` (profiles.py:124); ``profile`` measures
+  the (task, gamma) latency rows of profiles.py:82-121 on the device.
+
+Every forward goes through libtokadapt_cuda.so (ctypes); there is no PyTorch or CPU
+fallback for any stage of the path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple, Union
+
+import torch
+
+from . import _cuda
+from .config import PROMPT_MODES, ViTConfig, token_schedule
+from .core import Batch, us_from_s
+from .errors import ConfigError, ProfileGapError
+from .profiles import ProfileTable
+
+__all__ = ["TransformerModel", "TaskModel", "ServeModel"]
+
+_DTYPES = {"bf16": _cuda.DTYPE_BF16, "fp32": _cuda.DTYPE_F32}
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream_handle(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class TransformerModel:
+    """ViT backbone resident on one GPU.
+
+    params: fp32 CPU master weights (weights.init_backbone layout, = timm state dict).
+    dtype "bf16" runs the tcgen05 path; "fp32" is the parity mode (SIMT fp32 GEMMs).
+    """
+
+    def __init__(self, cfg: ViTConfig, params: Dict[str, object], device: Union[str, torch.device] = "cuda:0",
+                 dtype: str = "bf16", prompt_mode: str = "accumulate", n_tasks: int = 1,
+                 max_classes: int = 100):
+        if dtype not in _DTYPES:
+            raise ConfigError(f"dtype must be one of {sorted(_DTYPES)}")
+        if prompt_mode not in PROMPT_MODES:
+            raise ConfigError(f"prompt_mode must be one of {PROMPT_MODES}")
+        self.cfg, self.dtype, self.prompt_mode = cfg, dtype, prompt_mode
+        self.device = torch.device(device)
+        if self.device.type != "cuda":
+            raise ConfigError("TransformerModel runs on a CUDA device only (no CPU fallback)")
+        self.n_tasks, self.max_classes = n_tasks, max_classes
+        self._lib = _cuda.lib()
+        desc = _cuda.ModelDesc(cfg.dim, cfg.depth, cfg.heads, cfg.mlp_dim, cfg.patch, cfg.img,
+                               n_tasks, max_classes,
+                               _cuda.PROMPT_ACCUMULATE if prompt_mode == "accumulate" else _cuda.PROMPT_REPLACE,
+                               _DTYPES[dtype])
+        handle = ctypes.c_void_p()
+        _cuda.check(self._lib.ta_model_create(self.device.index or 0, ctypes.byref(desc), ctypes.byref(handle)))
+        self._h = handle
+        self._keep: List[torch.Tensor] = []
+        self._upload(params)
+        self._ws: Dict[Tuple[int, int], torch.Tensor] = {}
+
+    # -- weights -------------------------------------------------------------------
+    def _mat(self, w: torch.Tensor) -> torch.Tensor:
+        dt = torch.bfloat16 if self.dtype == "bf16" else torch.float32
+        t = w.to(device=self.device, dtype=dt).contiguous()
+        self._keep.append(t)
+        return t
+
+    def _vec(self, v: torch.Tensor) -> torch.Tensor:
+        t = v.to(device=self.device, dtype=torch.float32).contiguous()
+        self._keep.append(t)
+        return t
+
+    def _upload(self, p: Dict[str, object]) -> None:
+        cfg = self.cfg
+        pw = p["patch_w"].reshape(cfg.dim, cfg.patch_k)
+        if cfg.patch_k_padded != cfg.patch_k:
+            pw = torch.nn.functional.pad(pw, (0, cfg.patch_k_padded - cfg.patch_k))
+        layers = (_cuda.LayerWeights * cfg.depth)()
+        for i, lw in enumerate(p["layers"]):
+            vals = {}
+            for k in ("qkv_w", "proj_w", "fc1_w", "fc2_w"):
+                vals[k] = _ptr(self._mat(lw[k]))
+            for k in ("ln1_w", "ln1_b", "qkv_b", "proj_b", "ln2_w", "ln2_b", "fc1_b", "fc2_b"):
+                vals[k] = _ptr(self._vec(lw[k]))
+            layers[i] = _cuda.LayerWeights(**vals)
+        self._layers_c = layers
+        self._weights_c = _cuda.Weights(
+            _ptr(self._mat(pw)), _ptr(self._vec(p["patch_b"])), _ptr(self._vec(p["cls"])),
+            _ptr(self._vec(p["pos"])), _ptr(self._vec(p["norm_w"])), _ptr(self._vec(p["norm_b"])),
+            ctypes.cast(layers, ctypes.POINTER(_cuda.LayerWeights)))
+        _cuda.check(self._lib.ta_model_set_weights(self._h, ctypes.byref(self._weights_c)))
+
+    def set_head(self, task: int, w: torch.Tensor, b: torch.Tensor) -> None:
+        wt, bt = self._vec(w), self._vec(b)
+        _cuda.check(self._lib.ta_model_set_head(self._h, task, wt.data_ptr(), bt.data_ptr(), int(w.shape[0])))
+
+    def set_prompts(self, task: int, gamma: int, prompts: torch.Tensor) -> None:
+        cfg = self.cfg
+        if tuple(prompts.shape) != (cfg.depth, gamma, cfg.dim):
+            raise ValueError(f"prompts must be [L={cfg.depth}, gamma={gamma}, D={cfg.dim}]")
+        pt = self._vec(prompts)
+        _cuda.check(self._lib.ta_model_set_prompts(self._h, task, gamma, pt.data_ptr()))
+
+    # -- schedule / workspace --------------------------------------------------------
+    def schedule(self, gamma: int) -> Tuple[List[int], List[int]]:
+        return token_schedule(self.cfg, gamma, self.prompt_mode)
+
+    def workspace(self, batch: int, gamma: int) -> torch.Tensor:
+        key = (batch, gamma)
+        ws = self._ws.get(key)
+        if ws is None:
+            n = ctypes.c_size_t()
+            _cuda.check(self._lib.ta_workspace_size(self._h, batch, gamma, ctypes.byref(n)))
+            ws = torch.empty(n.value, dtype=torch.uint8, device=self.device)
+            self._ws[key] = ws
+        return ws
+
+    def trace_len(self, batch: int, gamma: int) -> int:
+        n = ctypes.c_size_t()
+        _cuda.check(self._lib.ta_merge_trace_len(self._h, batch, gamma, ctypes.byref(n)))
+        return n.value
+
+    # -- forward -------------------------------------------------------------------
+    def forward_raw(self, images: torch.Tensor, task_ids: torch.Tensor, gamma: int,
+                    logits: Optional[torch.Tensor] = None, trace: Optional[torch.Tensor] = None,
+                    forced_trace: Optional[torch.Tensor] = None,
+                    workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Device tensors in, device logits out; asynchronous on the current stream."""
+        b = images.shape[0]
+        if images.dtype != torch.float32 or not images.is_contiguous() or images.device != self.device:
+            raise ValueError("images must be contiguous fp32 on the model's device")
+        if task_ids.dtype != torch.int32 or task_ids.device != self.device:
+            raise ValueError("task ids must be int32 on the model's device")
+        if logits is None:
+            logits = torch.empty(b, self.max_classes, dtype=torch.float32, device=self.device)
+        ws = workspace if workspace is not None else self.workspace(b, gamma)
+        rc = self._lib.ta_forward(self._h, images.data_ptr(), task_ids.data_ptr(), b, gamma,
+                                  logits.data_ptr(), _ptr(trace), _ptr(forced_trace),
+                                  ws.data_ptr(), ws.numel(), _stream_handle(self.device))
+        _cuda.check(rc, gamma=gamma)
+        return logits
+
+    def forward_host(self, images: torch.Tensor, task_ids: torch.Tensor, gamma: int,
+                     out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Host (CPU, ideally pinned) tensors in and out through ta_forward_host."""
+        b = images.shape[0]
+        imgs = images.contiguous()
+        tids = task_ids.to(torch.int32).contiguous()
+        if out is None:
+            out = torch.empty(b, self.max_classes, dtype=torch.float32)
+        rc = self._lib.ta_forward_host(self._h, imgs.data_ptr(), tids.data_ptr(), b, gamma,
+                                       out.data_ptr(), _stream_handle(self.device))
+        _cuda.check(rc, gamma=gamma)
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            torch.cuda.synchronize(self.device)
+            self._lib.ta_model_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class TaskModel:
+    """Per-task parameters: head [C, D] + prompts per gamma [L, gamma, D]."""
+
+    name: str
+    head_w: torch.Tensor
+    head_b: torch.Tensor
+    prompts: Dict[int, torch.Tensor] = field(default_factory=dict)
+
+    @property
+    def classes(self) -> int:
+        return int(self.head_w.shape[0])
+
+
+class ServeModel:
+    """Front end over one backbone replica and its registered tasks."""
+
+    def __init__(self, backbone: TransformerModel, tasks: Sequence[TaskModel] = ()):
+        self.backbone = backbone
+        self.tasks: List[TaskModel] = []
+        self.task_index: Dict[str, int] = {}
+        for t in tasks:
+            self.register_task(t)
+
+    def register_task(self, task: TaskModel) -> int:
+        """Register_Task: head + prompt repository entries."""
+        if task.name in self.task_index:
+            raise ConfigError(f"task {task.name!r} already registered")
+        idx = len(self.tasks)
+        if idx >= self.backbone.n_tasks:
+            raise ConfigError(f"backbone was built for {self.backbone.n_tasks} tasks")
+        if task.classes > self.backbone.max_classes:
+            raise ConfigError(f"task {task.name!r} has {task.classes} classes > max_classes")
+        self.backbone.set_head(idx, task.head_w, task.head_b)
+        for gamma, p in task.prompts.items():
+            self.backbone.set_prompts(idx, gamma, p)
+        self.tasks.append(task)
+        self.task_index[task.name] = idx
+        return idx
+
+    def task_ids(self, tasks: Union[Sequence[str], Sequence[int], torch.Tensor]) -> torch.Tensor:
+        if isinstance(tasks, torch.Tensor):
+            ids = tasks.to(torch.int32)
+        else:
+            ids = torch.tensor([self.task_index[t] if isinstance(t, str) else int(t) for t in tasks],
+                               dtype=torch.int32)
+        return ids
+
+    def _check_gamma(self, ids_host: torch.Tensor, gamma: int) -> None:
+        if gamma < -(self.backbone.cfg.n_tokens - 1):
+            raise ValueError(f"gamma {gamma} merges more tokens than exist")
+        if gamma > 0:
+            for i in set(ids_host.tolist()):
+                if i < 0 or i >= len(self.tasks):
+                    raise ValueError(f"unknown task id {i}")
+                if gamma not in self.tasks[i].prompts:
+                    raise ProfileGapError(self.tasks[i].name, gamma, "prompt")
+
+    def forward(self, inputs: torch.Tensor, tasks, task_params=None, gamma: int = 0) -> torch.Tensor:
+        """ServeModel.forward(inputs, tasks, task_params, gamma).
+
+        inputs [B, 3, S, S] fp32 (device or host); tasks = names / ids / int tensor;
+        task_params (optional) TaskModels to register first.  Returns logits
+        [B, max_classes] on the inputs' device, -inf beyond each task's class count.
+        """
+        if task_params:
+            for tp in task_params:
+                if tp.name not in self.task_index:
+                    self.register_task(tp)
+        ids = self.task_ids(tasks)
+        self._check_gamma(ids.cpu(), gamma)
+        if inputs.device.type == "cpu":
+            return self.backbone.forward_host(inputs.float(), ids, gamma)
+        return self.backbone.forward_raw(inputs.float().contiguous(), ids.to(self.backbone.device), gamma)
+
+    __call__ = forward
+
+    def execute(self, batch: Batch, gamma: int, payloads: Dict[int, torch.Tensor]) -> Tuple[int, List[int]]:
+        """Run a planned batch (engine step) and return (latency_us, predictions).
+
+        payloads maps query id -> image [3, S, S]; Batch itself carries metadata only
+        (SPEC.md:90).  Latency is device time (CUDA events) in integer microseconds, the
+        unit of the whole scheduler (core.py:3-5).
+        """
+        imgs = torch.stack([payloads[q.id] for q in batch.queries]).to(self.backbone.device, torch.float32)
+        ids = self.task_ids([q.task for q in batch.queries])
+        self._check_gamma(ids, gamma)
+        ids_dev = ids.to(self.backbone.device)
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record()
+        logits = self.backbone.forward_raw(imgs.contiguous(), ids_dev, gamma)
+        end.record()
+        end.synchronize()
+        latency_us = us_from_s(start.elapsed_time(end) / 1e3)
+        preds = []
+        for i, q in enumerate(batch.queries):
+            c = self.tasks[self.task_index[q.task]].classes
+            preds.append(int(logits[i, :c].argmax().item()))
+        return latency_us, preds
+
+    def profile(self, gammas: Sequence[int], batch_size: int, accuracy: Optional[Dict[Tuple[str, int], float]] = None,
+                iters: int = 5, warmup: int = 2, seed: int = 0) -> ProfileTable:
+        """B200 task profiler: measure per-sample and
+        per-batch latency for every registered task at each gamma and return a
+        ProfileTable (write it with profiles.write_profile_csv)."""
+        table = ProfileTable(base_tokens=self.backbone.cfg.n_tokens, layers=self.backbone.cfg.depth)
+        cfg = self.backbone.cfg
+        g = torch.Generator(device=self.backbone.device).manual_seed(seed)
+        imgs = torch.randn(batch_size, 3, cfg.img, cfg.img, generator=g, device=self.backbone.device)
+        for gamma in gammas:
+            batch_times = []
+            for ti, task in enumerate(self.tasks):
+                if gamma > 0 and gamma not in task.prompts:
+                    continue
+                ids = torch.full((batch_size,), ti, dtype=torch.int32, device=self.backbone.device)
+                for _ in range(warmup):
+                    self.backbone.forward_raw(imgs, ids, gamma)
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                for _ in range(iters):
+                    self.backbone.forward_raw(imgs, ids, gamma)
+                e.record()
+                e.synchronize()
+                sec = s.elapsed_time(e) / 1e3 / iters
+                batch_times.append(sec)
+                table.sample_latency_us[(task.name, gamma)] = max(1, us_from_s(sec / batch_size))
+                table.accuracy[(task.name, gamma)] = (accuracy or {}).get((task.name, gamma), 1.0)
+            if batch_times:
+                table.batch_latency_us[(gamma, batch_size)] = max(1, us_from_s(sum(batch_times) / len(batch_times)))
+        return table
