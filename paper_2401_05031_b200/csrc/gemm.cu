@@ -23,69 +23,106 @@
 namespace ta {
 
 // ------------------------------------------------------------------ epilogue
-template <int EPI, typename OutT>
-__device__ __forceinline__ void epi_store32(const GemmEpi& e, int N, long long m, int n0,
-                                            float (&v)[32]) {
-  const long long orow = epi_out_row(e, m);
-  const float4* b4 = reinterpret_cast<const float4*>(e.bias + n0);
+// One epilogue warp owns TMEM lanes [32*q, 32*q + 32) (q = warp % 4) and a 128-column
+// half of the 256-wide accumulator.  Per 32-column chunk: tcgen05.ld (thread = row) ->
+// swizzled smem transpose -> each lane handles 4 consecutive columns of 8 rows, so bias,
+// residual loads and output stores are coalesced 16-byte accesses along the row.
+// The chunk loop is software-pipelined: chunk c+1's transpose and residual loads are
+// issued before chunk c's stores (out may alias resid, but only element-for-element).
+struct EpiChunk {
+  float4 v[8];
+  float4 x[8];  // residual / positional rows, added at store time so loads stay in flight
+};
+
+template <int EPI>
+__device__ __forceinline__ void epi_load(const GemmEpi& e, int M, int N, long long m_base, int n0,
+                                         const uint32_t (&r)[32], float4* stage, EpiChunk& c) {
+  const uint32_t lane = lane_id();
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float4 b = __ldg(b4 + j);
-    v[4 * j + 0] += b.x;
-    v[4 * j + 1] += b.y;
-    v[4 * j + 2] += b.z;
-    v[4 * j + 3] += b.w;
+  for (int q = 0; q < 8; ++q) {
+    float4 v = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                           __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+    stage[lane * 8 + (q ^ (lane & 7))] = v;
   }
-  if constexpr (EPI == EPI_BIAS_GELU) {
+  __syncwarp();
+  const int g = lane & 7;
+  const int n = n0 + 4 * g;
+  const int row0 = lane >> 3;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+  for (int k = 0; k < 8; ++k) {
+    const int row = row0 + 4 * k;
+    c.v[k] = stage[row * 8 + (g ^ (row & 7))];
   }
+  __syncwarp();
+  const bool full = m_base + 32 <= M;
   if constexpr (EPI == EPI_BIAS_RESID) {
-    const float4* r4 = reinterpret_cast<const float4*>(e.resid + m * N + n0);
+    const float* rp = e.resid + (m_base + row0) * N + n;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float4 r = r4[j];
-      v[4 * j + 0] += r.x;
-      v[4 * j + 1] += r.y;
-      v[4 * j + 2] += r.z;
-      v[4 * j + 3] += r.w;
+    for (int k = 0; k < 8; ++k) {
+      if (full || m_base + row0 + 4 * k < M) {
+        c.x[k] = *reinterpret_cast<const float4*>(rp + static_cast<long long>(4 * k) * N);
+      }
     }
   }
   if constexpr (EPI == EPI_PATCH) {
-    const long long prow = e.row_off + (m % e.rows_in);
-    const float4* p4 = reinterpret_cast<const float4*>(e.pos + prow * N + n0);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float4 p = __ldg(p4 + j);
-      v[4 * j + 0] += p.x;
-      v[4 * j + 1] += p.y;
-      v[4 * j + 2] += p.z;
-      v[4 * j + 3] += p.w;
+    for (int k = 0; k < 8; ++k) {
+      const long long m = m_base + row0 + 4 * k;
+      if (m < M) {
+        c.x[k] =
+            __ldg(reinterpret_cast<const float4*>(e.pos + (e.row_off + (m % e.rows_in)) * N + n));
+      }
     }
   }
-  if constexpr (sizeof(OutT) == 2) {
-    uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(e.out) + orow * N + n0);
+}
+
+template <int EPI, typename OutT, bool kRemap>
+__device__ __forceinline__ void epi_store(const GemmEpi& e, int M, int N, long long m_base, int n0,
+                                          const EpiChunk& c) {
+  const uint32_t lane = lane_id();
+  const int n = n0 + 4 * (lane & 7);
+  const int row0 = lane >> 3;
+  const float4 b = __ldg(reinterpret_cast<const float4*>(e.bias + n));
+  const bool full = m_base + 32 <= M;
+  OutT* obase = static_cast<OutT*>(e.out);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      uint4 w;
-      w.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
-      w.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
-      w.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
-      w.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
-      o[j] = w;
+  for (int k = 0; k < 8; ++k) {
+    const long long m = m_base + row0 + 4 * k;
+    if (!full && m >= M) continue;
+    float4 w = c.v[k];
+    w.x += b.x;
+    w.y += b.y;
+    w.z += b.z;
+    w.w += b.w;
+    if constexpr (EPI == EPI_BIAS_RESID || EPI == EPI_PATCH) {
+      w.x += c.x[k].x;
+      w.y += c.x[k].y;
+      w.z += c.x[k].z;
+      w.w += c.x[k].w;
     }
-  } else {
-    float4* o = reinterpret_cast<float4*>(static_cast<float*>(e.out) + orow * N + n0);
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      o[j] = make_float4(v[4 * j + 0], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    if constexpr (EPI == EPI_BIAS_GELU) {
+      w.x = gelu_erf_fast(w.x);
+      w.y = gelu_erf_fast(w.y);
+      w.z = gelu_erf_fast(w.z);
+      w.w = gelu_erf_fast(w.w);
+    }
+    const long long orow = kRemap ? epi_out_row(e, m) : m;
+    if constexpr (sizeof(OutT) == 2) {
+      uint2 pk;
+      pk.x = pack_bf16(w.x, w.y);
+      pk.y = pack_bf16(w.z, w.w);
+      *reinterpret_cast<uint2*>(obase + orow * N + n) = pk;
+    } else {
+      *reinterpret_cast<float4*>(obase + orow * N + n) = w;
+    }
   }
 }
 
 // ------------------------------------------------------------------ tcgen05 kernel
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 B rows -> SWIZZLE_128B
-constexpr int kGemmThreads = 256;
+constexpr int kEpiWarps = 8;
+constexpr int kGemmThreads = 128 + 32 * kEpiWarps;
 
 template <int BN>
 struct GemmCfg {
@@ -94,10 +131,11 @@ struct GemmCfg {
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;  // two accumulator stages
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kEpiBytes = kEpiWarps * 32 * 32 * 4;  // per-warp 32x32 fp32 transpose
+  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 256;
 };
 
-template <int BN, int EPI, typename OutT>
+template <int BN, int EPI, typename OutT, bool kRemap>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_bf16_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
@@ -107,7 +145,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  float4* epi_stage = reinterpret_cast<float4*>(smem + S * Cfg::kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -127,7 +166,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 32 * kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -203,31 +242,52 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    const uint32_t ew = warp - 4;  // == warp % 4: TMEM lanes [32*ew, 32*ew + 32)
+    const uint32_t ew = warp - 4;
+    const uint32_t q = ew & 3;               // TMEM lane quarter (== warp % 4)
+    const int col0 = (ew >> 2) * (BN / 2);   // column half owned by this warp
+    constexpr int kChunks = BN / 2 / 32;
+    float4* stage = epi_stage + ew * 256;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int m_blk = tile / num_n;
       const int n_blk = tile - m_blk * num_n;
+      const long long m_base = static_cast<long long>(m_blk) * kBM + q * 32;
+      if constexpr (EPI == EPI_BIAS_RESID) {
+        // Pull this warp's residual rows (32 x BN/2 fp32) into L2 while the MMAs run.
+        const long long m = m_base + lane;
+        if (m < M)
+          prefetch_l2_bulk(epi.resid + m * N + n_blk * BN + col0, BN / 2 * sizeof(float));
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const long long m = static_cast<long long>(m_blk) * kBM + ew * 32 + lane;
-      const uint32_t t_row = tmem_base + ((ew * 32u) << 16) + acc * BN;
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * BN + col0;
+      uint32_t r0[32], r1[32];
+      EpiChunk ca, cb;
+      const bool live = m_base < M;
+      const int nb = n_blk * BN + col0;
+      static_assert(kChunks % 2 == 0, "chunk pairs");
+      tmem_ld_32x32b_x32(t_row, r0);
+      tmem_ld_wait();
+      if (live) epi_load<EPI>(epi, M, N, m_base, nb, r0, stage, ca);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_row + c * 32, r);
+      for (int c = 0; c < kChunks; c += 2) {
+        tmem_ld_32x32b_x32(t_row + (c + 1) * 32, r1);
         tmem_ld_wait();
-        if (c == BN / 32 - 1) {
+        if (c + 2 == kChunks) {
           tc_fence_before();
           mbar_arrive(&tempty[acc]);
         }
-        if (m < M) {
-          float v[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          epi_store32<EPI, OutT>(epi, N, m, n_blk * BN + c * 32, v);
+        if (live) {
+          epi_load<EPI>(epi, M, N, m_base, nb + (c + 1) * 32, r1, stage, cb);
+          epi_store<EPI, OutT, kRemap>(epi, M, N, m_base, nb + c * 32, ca);
         }
+        if (c + 2 < kChunks) {
+          tmem_ld_32x32b_x32(t_row + (c + 2) * 32, r0);
+          tmem_ld_wait();
+          if (live) epi_load<EPI>(epi, M, N, m_base, nb + (c + 2) * 32, r0, stage, ca);
+        }
+        if (live) epi_store<EPI, OutT, kRemap>(epi, M, N, m_base, nb + (c + 1) * 32, cb);
       }
       if (++acc == 2) {
         acc = 0;
@@ -345,11 +405,11 @@ int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_
   return r == CUDA_SUCCESS ? TA_OK : TA_ERR_SHAPE;
 }
 
-template <int BN, int EPI, typename OutT>
+template <int BN, int EPI, typename OutT, bool kRemap = false>
 static int launch_bf16(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, int N, int K,
                        const GemmEpi& epi, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
-  auto kern = gemm_bf16_sm100_kernel<BN, EPI, OutT>;
+  auto kern = gemm_bf16_sm100_kernel<BN, EPI, OutT, kRemap>;
   static bool attr_set = false;  // per instantiation; benign race (idempotent)
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -384,9 +444,10 @@ static int dispatch_bf16(const CUtensorMap& a, const CUtensorMap& b, int M, int 
       return out_bf16 ? launch_bf16<BN, EPI_BIAS_GELU, __nv_bfloat16>(a, b, M, N, K, epi, s)
                       : launch_bf16<BN, EPI_BIAS_GELU, float>(a, b, M, N, K, epi, s);
     case EPI_BIAS_RESID:
-      return launch_bf16<BN, EPI_BIAS_RESID, float>(a, b, M, N, K, epi, s);
+      return epi.rows_in ? launch_bf16<BN, EPI_BIAS_RESID, float, true>(a, b, M, N, K, epi, s)
+                         : launch_bf16<BN, EPI_BIAS_RESID, float, false>(a, b, M, N, K, epi, s);
     case EPI_PATCH:
-      return launch_bf16<BN, EPI_PATCH, float>(a, b, M, N, K, epi, s);
+      return launch_bf16<BN, EPI_PATCH, float, true>(a, b, M, N, K, epi, s);
   }
   return TA_ERR_INVALID;
 }

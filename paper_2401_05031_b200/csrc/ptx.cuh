@@ -80,6 +80,13 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* ba
       : "memory");
 }
 
+// Bulk prefetch of [ptr, ptr + bytes) into L2 (bytes multiple of 16, 16-byte aligned).
+__device__ __forceinline__ void prefetch_l2_bulk(const void* ptr, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(ptr)),
+               "r"(bytes)
+               : "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
@@ -214,6 +221,33 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 }
 __device__ __forceinline__ float gelu_erf(float x) {
   return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+}
+// erf-GELU with erf from Abramowitz & Stegun 7.1.26 (|err| <= 1.5e-7): one SFU reciprocal,
+// one SFU exp, five FMAs — used by the bf16 tensor-core epilogues, where libm erff made
+// the fc1 epilogue slower than its MMAs.  fp32 parity mode keeps erff (gelu_erf).
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float gelu_erf_fast(float x) {
+  // z = |x| / sqrt(2);  exp(-z^2) = 2^(-(|x| * sqrt(log2(e) / 2))^2)
+  const float a = fabsf(x);
+  const float t = rcp_approx(fmaf(0.3275911f * 0.70710678118654752f, a, 1.0f));
+  float p = fmaf(1.061405429f, t, -1.453152027f);
+  p = fmaf(p, t, 1.421413741f);
+  p = fmaf(p, t, -0.284496736f);
+  p = fmaf(p, t, 0.254829592f);
+  p *= t;
+  const float u = a * 0.84932180028801904f;  // sqrt(log2(e) / 2)
+  const float erf_abs = fmaf(-p, ex2_approx(-u * u), 1.0f);
+  const float hx = 0.5f * x;
+  return fmaf(hx, copysignf(erf_abs, x), hx);
 }
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

@@ -11,42 +11,57 @@ namespace ta {
 
 // ------------------------------------------------------------------ patchify
 // out[b*Np + py*G + px, c*P*P + ky*P + kx] = img[b, c, py*P + ky, px*P + kx]; cols >= 3P^2 zero.
+// One CTA per (patch row py, image b): the 3 x P x S input strip is read once, coalesced,
+// into smem; the G x Kp output block is written with consecutive threads on consecutive
+// columns (two elements per thread).
 template <typename T>
-__global__ void patchify_kernel(const float* __restrict__ img, T* __restrict__ out, int B, int S,
-                                int P, int Kp) {
+__global__ void __launch_bounds__(256) patchify_kernel(const float* __restrict__ img,
+                                                       T* __restrict__ out, int S, int P, int Kp) {
+  extern __shared__ float strip[];  // [3][P][S]
+  const int py = blockIdx.x, b = blockIdx.y;
   const int G = S / P;
-  const int Np = G * G;
   const int K = 3 * P * P;
-  const long long total = static_cast<long long>(B) * Np * Kp;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int col = static_cast<int>(i % Kp);
-    const long long row = i / Kp;
-    float v = 0.f;
-    if (col < K) {
-      const int b = static_cast<int>(row / Np);
-      const int p = static_cast<int>(row % Np);
-      const int py = p / G, px = p % G;
-      const int c = col / (P * P);
-      const int rem = col % (P * P);
-      const int ky = rem / P, kx = rem % P;
-      v = img[((static_cast<long long>(b) * 3 + c) * S + py * P + ky) * S + px * P + kx];
+  const int n4 = 3 * P * S / 4;
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+    const int e = 4 * i;
+    const int c = e / (P * S), rem = e % (P * S);
+    const int ky = rem / S, x = rem % S;
+    reinterpret_cast<float4*>(strip)[i] = *reinterpret_cast<const float4*>(
+        img + ((static_cast<long long>(b) * 3 + c) * S + py * P + ky) * S + x);
+  }
+  __syncthreads();
+  T* ob = out + (static_cast<long long>(b) * G * G + static_cast<long long>(py) * G) * Kp;
+  const int total2 = G * Kp / 2;
+  for (int i = threadIdx.x; i < total2; i += blockDim.x) {
+    float v[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int idx = 2 * i + u;
+      const int px = idx / Kp, col = idx % Kp;
+      float val = 0.f;
+      if (col < K) {
+        const int c = col / (P * P), rem = col % (P * P);
+        const int ky = rem / P, kx = rem % P;
+        val = strip[(c * P + ky) * S + px * P + kx];
+      }
+      v[u] = val;
     }
     if constexpr (sizeof(T) == 2)
-      out[i] = __float2bfloat16_rn(v);
+      reinterpret_cast<uint32_t*>(ob)[i] = pack_bf16(v[0], v[1]);
     else
-      out[i] = v;
+      reinterpret_cast<float2*>(ob)[i] = make_float2(v[0], v[1]);
   }
 }
 
 int patchify(const float* img, void* out, int B, int S, int P, int Kp, int dtype,
              cudaStream_t s) {
-  const long long total = static_cast<long long>(B) * (S / P) * (S / P) * Kp;
-  const int grid = static_cast<int>((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+  if (S % 4 != 0 || Kp % 2 != 0) return TA_ERR_SHAPE;
+  const size_t smem = static_cast<size_t>(3) * P * S * sizeof(float);
+  dim3 grid(S / P, B);
   if (dtype == TA_DTYPE_BF16)
-    patchify_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(img, static_cast<__nv_bfloat16*>(out), B, S, P, Kp);
+    patchify_kernel<__nv_bfloat16><<<grid, 256, smem, s>>>(img, static_cast<__nv_bfloat16*>(out), S, P, Kp);
   else
-    patchify_kernel<float><<<grid, 256, 0, s>>>(img, static_cast<float*>(out), B, S, P, Kp);
+    patchify_kernel<float><<<grid, 256, smem, s>>>(img, static_cast<float*>(out), S, P, Kp);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
