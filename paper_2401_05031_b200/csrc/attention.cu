@@ -8,6 +8,7 @@
 // in fp32 registers, m16n8k16 bf16 MMAs.
 // fp32: SIMT reference-precision kernel for the fp32 parity mode.
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.h"
 #include "ptx.cuh"
@@ -292,10 +293,25 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// 0 = tcgen05 kernel where it applies (default), 1 = force the mma.sync kernel
+// (TA_ATTENTION_BACKEND=mma; used by the parity tests to cover both kernels).
+static int attention_backend() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* v = getenv("TA_ATTENTION_BACKEND");
+    mode = (v && v[0] == 'm') ? 1 : 0;
+  }
+  return mode;
+}
+
 int attention(const void* qkv, const float* size, int B, int t, int H, int hd, void* out,
               int dtype, cudaStream_t s) {
   if (t <= 0) return TA_OK;
   cudaError_t e;
+  if (dtype == TA_DTYPE_BF16 && attention_backend() == 0) {
+    const int rc = attention_tc(qkv, size, B, t, H, hd, out, s);
+    if (rc != TA_ERR_SHAPE) return rc;  // outside the tcgen05 envelope -> mma.sync below
+  }
   if (dtype == TA_DTYPE_BF16) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((t + 63) / 64, H, B);

@@ -1,0 +1,407 @@
+// Proportional attention on the 5th-gen tensor cores (north_star 3):
+//   o = softmax(q k^T / sqrt(hd) + log size_j) v        per (image, head), hd = 64, t <= 512
+//
+// Persistent, warp-specialised, one CTA per SM looping over work items (image, head); each
+// item walks its 128-query tiles with K / V fetched from HBM once per item.
+//   warp 8 (lane 0)  TMA producer: K, V of the item (64-row SW128 boxes) into a 2-slot
+//                    ring (1 slot when t > 256), Q tiles into a 2-slot ring.
+//   warp 9 (lane 0)  MMA issuer: S = Q K^T (M = 128, N <= 256 per instruction) into one of
+//                    two TMEM S slots; S of tile n+1 is issued before PV of tile n so the
+//                    softmax warps never wait for it; O += P_blk V_blk per 64-key block with
+//                    V as an MN-major B operand.
+//   warps 0..7       softmax in two groups over even / odd 64-key blocks; query row i is
+//                    TMEM lane i (warps w and w+4 share lanes 32(w%4)..); pass 1 row max of
+//                    s * log2(e)/sqrt(hd) + log2(size_j), pass 2 p = 2^(v - max) -> bf16 P
+//                    block into ring stage g (SW128, K-major) -> PV MMA; row max / sum
+//                    combined through smem; epilogue O / sum -> bf16 rows.
+// TMEM: slot s at columns [256 s, 256 s + t_pad); O aliases the slot's S block 0, which
+// softmax has consumed before the first PV MMA is issued.  Keys past t are masked with a
+// -inf bias (their K / V rows are the next image's rows or TMA zero fill: finite, p = 0).
+#include <cfloat>
+
+#include <cudaTypedefs.h>
+
+#include "common.h"
+#include "ptx.cuh"
+
+namespace ta {
+
+int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                      uint32_t box_rows);
+
+namespace {
+
+constexpr int kHd = 64;
+constexpr int kQTile = 128;
+constexpr int kKeyBlk = 64;
+constexpr int kBlkBytes = kKeyBlk * kHd * 2;  // 8 KB: one 64-row SW128 box
+constexpr int kQBytes = kQTile * kHd * 2;     // 16 KB
+constexpr int kPBytes = kQTile * kKeyBlk * 2;  // 16 KB: one P block
+constexpr int kMaxTPad = 512;
+constexpr int kThreads = 320;
+
+struct AttnTcLayout {
+  int t_pad;    // round_up(t, 64)
+  int n_kb;     // t_pad / 64
+  int n_qt;     // ceil(t / 128)
+  int n_kv;     // K/V ring slots (2 when t_pad <= 256)
+  int n_s;      // TMEM S slots (2 when t_pad <= 256)
+  uint32_t kv_bytes;  // per slot: K then V
+  uint32_t kv_off, p_off, bias_off, red_off, bar_off, smem_bytes;
+};
+
+AttnTcLayout attn_layout(int t) {
+  AttnTcLayout L{};
+  L.t_pad = (t + kKeyBlk - 1) / kKeyBlk * kKeyBlk;
+  L.n_kb = L.t_pad / kKeyBlk;
+  L.n_qt = (t + kQTile - 1) / kQTile;
+  L.n_kv = L.t_pad <= 256 ? 2 : 1;
+  L.n_s = L.t_pad <= 256 ? 2 : 1;
+  L.kv_bytes = 2u * L.n_kb * kBlkBytes;
+  uint32_t off = 2 * kQBytes;  // Q ring
+  L.kv_off = off;
+  off += L.n_kv * L.kv_bytes;
+  L.p_off = off;
+  off += 2 * kPBytes;
+  L.bias_off = off;
+  off += kMaxTPad * 4;
+  L.red_off = off;
+  off += 4 * 128 * 4;
+  L.bar_off = off;
+  off += 32 * 8;
+  L.smem_bytes = off + 1024;  // + alignment slack
+  return L;
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const float* __restrict__ size, int t,
+                   int H, int n_items, __nv_bfloat16* __restrict__ out, float scale_log2,
+                   AttnTcLayout L) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  const int D = H * kHd;
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + L.kv_off;
+  uint8_t* sP = smem + L.p_off;
+  float* bias = reinterpret_cast<float*>(smem + L.bias_off);
+  float* red = reinterpret_cast<float*>(smem + L.red_off);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+  uint64_t* kv_full = bars + 0;   // [2]
+  uint64_t* kv_free = bars + 2;   // [2]
+  uint64_t* q_full = bars + 4;    // [2]
+  uint64_t* q_free = bars + 6;    // [2]
+  uint64_t* s_full = bars + 8;    // [2]
+  uint64_t* s_free = bars + 10;   // [2]
+  uint64_t* o_full = bars + 12;   // [2]
+  uint64_t* p_full = bars + 14;   // [2]
+  uint64_t* p_free = bars + 16;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&tm);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_free[s], 1);
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_free[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_free[s], 256);
+      mbar_init(&o_full[s], 1);
+      mbar_init(&p_full[s], 128);
+      mbar_init(&p_free[s], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  grid_dep_wait();  // qkv is the previous kernel's output
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      uint32_t it = 0, qcnt = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        const int b = item / H, h = item - b * H;
+        const int row_base = b * t;
+        const int kvs = it % L.n_kv;
+        const uint32_t kv_use = it / L.n_kv;
+        mbar_wait(&kv_free[kvs], (kv_use & 1) ^ 1);
+        uint8_t* sK = sKV + kvs * L.kv_bytes;
+        uint8_t* sV = sK + L.n_kb * kBlkBytes;
+        mbar_arrive_expect_tx(&kv_full[kvs], L.kv_bytes);
+        for (int kb = 0; kb < L.n_kb; ++kb) {
+          tma_load_2d(&tm, &kv_full[kvs], sK + kb * kBlkBytes, D + h * kHd, row_base + kb * kKeyBlk);
+          tma_load_2d(&tm, &kv_full[kvs], sV + kb * kBlkBytes, 2 * D + h * kHd, row_base + kb * kKeyBlk);
+        }
+        for (int qt = 0; qt < L.n_qt; ++qt, ++qcnt) {
+          const int qs = qcnt & 1;
+          mbar_wait(&q_free[qs], ((qcnt >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&q_full[qs], kQBytes);
+          tma_load_2d(&tm, &q_full[qs], sQ + qs * kQBytes, h * kHd, row_base + qt * kQTile);
+          tma_load_2d(&tm, &q_full[qs], sQ + qs * kQBytes + kBlkBytes, h * kHd,
+                      row_base + qt * kQTile + 64);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_pv = idesc_bf16(kQTile, kHd, /*b_mn_major=*/true);
+      uint32_t p_use[2] = {0, 0};
+      // pending PV tile (issued after the next tile's S so softmax never waits)
+      int pend_slot = -1, pend_kvs = 0;
+      bool pend_last = false;
+      auto issue_pv = [&](int sslot, int kvs, bool last_of_item) {
+        const uint8_t* sV = sKV + kvs * L.kv_bytes + L.n_kb * kBlkBytes;
+        const uint32_t o_tmem = tmem + sslot * 256;
+        for (int kb = 0; kb < L.n_kb; ++kb) {
+          const int ps = kb & 1;
+          mbar_wait(&p_full[ps], p_use[ps]++ & 1);
+          tc_fence_after();
+          const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
+          const uint32_t vbase = smem_u32(sV + kb * kBlkBytes);
+#pragma unroll
+          for (int kc = 0; kc < kKeyBlk / 16; ++kc) {
+            // V rows (keys) are the K dimension: 16 keys = two 8-row groups = 2048 B.
+            const uint64_t vdesc = umma_desc_sw128_mn(vbase + kc * 2048, 8192, 1024);
+            umma_f16(o_tmem, pdesc + 2 * kc, vdesc, idesc_pv, (kb | kc) != 0);
+          }
+          umma_commit(&p_free[ps]);
+        }
+        umma_commit(&o_full[sslot]);
+        if (last_of_item) umma_commit(&kv_free[kvs]);
+      };
+      uint32_t it = 0, qcnt = 0, tcnt = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        const int kvs = it % L.n_kv;
+        const uint32_t kv_use = it / L.n_kv;
+        const uint8_t* sK = sKV + kvs * L.kv_bytes;
+        for (int qt = 0; qt < L.n_qt; ++qt, ++qcnt, ++tcnt) {
+          const int qs = qcnt & 1;
+          const int ss = tcnt % L.n_s;
+          if (L.n_s == 1 && pend_slot >= 0) {  // single S slot: finish the previous tile first
+            issue_pv(pend_slot, pend_kvs, pend_last);
+            pend_slot = -1;
+          }
+          mbar_wait(&s_free[ss], ((tcnt / L.n_s) & 1) ^ 1);
+          mbar_wait(&q_full[qs], (qcnt >> 1) & 1);
+          if (qt == 0) mbar_wait(&kv_full[kvs], kv_use & 1);
+          tc_fence_after();
+          const uint64_t qdesc = umma_desc_sw128(smem_u32(sQ + qs * kQBytes));
+          for (int n0 = 0; n0 < L.t_pad; n0 += 256) {
+            const int n = L.t_pad - n0 < 256 ? L.t_pad - n0 : 256;
+            const uint32_t idesc_s = idesc_bf16(kQTile, n);
+            const uint64_t kdesc = umma_desc_sw128(smem_u32(sK + n0 * 128));
+#pragma unroll
+            for (int k = 0; k < kHd / 16; ++k)
+              umma_f16(tmem + ss * 256 + n0, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0);
+          }
+          umma_commit(&s_full[ss]);
+          umma_commit(&q_free[qs]);
+          if (pend_slot >= 0) issue_pv(pend_slot, pend_kvs, pend_last);
+          pend_slot = ss;
+          pend_kvs = kvs;
+          pend_last = qt + 1 == L.n_qt;
+        }
+      }
+      if (pend_slot >= 0) issue_pv(pend_slot, pend_kvs, pend_last);
+    }
+  } else {
+    // ------------------------------------------------------------ softmax / epilogue
+    // Per tile: pass 1 (row max), pass 2 (P blocks), epilogue (O / sum).  With two S slots
+    // the epilogue of tile n runs after pass 1 of tile n+1, hiding the PV completion latency.
+    const int g = warp >> 2;
+    const int i = (warp & 3) * 32 + lane;  // query row within the tile
+    const uint32_t lane_base = tmem + (((warp & 3) * 32u) << 16);
+    uint32_t use = 0;
+
+    // shared-space addresses (explicit ld/st.shared; see lds_f4)
+    const uint32_t s_bias = smem_u32(bias);
+    const uint32_t s_red = smem_u32(red);
+    const uint32_t s_prow = smem_u32(sP) + g * kPBytes + i * 128;
+
+    auto pass1 = [&](uint32_t tcnt) -> float {
+      const int ss = tcnt % L.n_s;
+      const uint32_t la = lane_base + ss * 256;
+      mbar_wait(&s_full[ss], (tcnt / L.n_s) & 1);
+      tc_fence_after();
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      for (int kb = g; kb < L.n_kb; kb += 2) {
+        uint32_t r[64];
+        tmem_ld_32x32b_x32(la + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+        tmem_ld_32x32b_x32(la + kb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 64; j += 4) {
+          const float4 bb = lds_f4(s_bias + (kb * 64 + j) * 4);
+          m4[0] = fmaxf(m4[0], fmaf(__uint_as_float(r[j]), scale_log2, bb.x));
+          m4[1] = fmaxf(m4[1], fmaf(__uint_as_float(r[j + 1]), scale_log2, bb.y));
+          m4[2] = fmaxf(m4[2], fmaf(__uint_as_float(r[j + 2]), scale_log2, bb.z));
+          m4[3] = fmaxf(m4[3], fmaf(__uint_as_float(r[j + 3]), scale_log2, bb.w));
+        }
+      }
+      sts_f32(s_red + (g * 128 + i) * 4, fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])));
+      named_bar_sync(1, 256);
+      return fmaxf(lds_f32(s_red + i * 4), lds_f32(s_red + (128 + i) * 4));
+    };
+
+    auto pass2 = [&](uint32_t tcnt, float mx) -> float {
+      const uint32_t la = lane_base + (tcnt % L.n_s) * 256;
+      float s4[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int kb = g; kb < L.n_kb; kb += 2, ++use) {
+        uint32_t r[64];
+        tmem_ld_32x32b_x32(la + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+        tmem_ld_32x32b_x32(la + kb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+        mbar_wait(&p_free[g], (use & 1) ^ 1);
+        tmem_ld_wait();
+#pragma unroll
+        for (int chunk = 0; chunk < 8; ++chunk) {  // 8 keys = one 16-byte chunk of the P row
+          const float4 b0 = lds_f4(s_bias + (kb * 64 + chunk * 8) * 4);
+          const float4 b1 = lds_f4(s_bias + (kb * 64 + chunk * 8 + 4) * 4);
+          const uint32_t* rr = &r[chunk * 8];
+          const float p0 = ex2_approx(fmaf(__uint_as_float(rr[0]), scale_log2, b0.x) - mx);
+          const float p1 = ex2_approx(fmaf(__uint_as_float(rr[1]), scale_log2, b0.y) - mx);
+          const float p2 = ex2_approx(fmaf(__uint_as_float(rr[2]), scale_log2, b0.z) - mx);
+          const float p3 = ex2_approx(fmaf(__uint_as_float(rr[3]), scale_log2, b0.w) - mx);
+          const float p4 = ex2_approx(fmaf(__uint_as_float(rr[4]), scale_log2, b1.x) - mx);
+          const float p5 = ex2_approx(fmaf(__uint_as_float(rr[5]), scale_log2, b1.y) - mx);
+          const float p6 = ex2_approx(fmaf(__uint_as_float(rr[6]), scale_log2, b1.z) - mx);
+          const float p7 = ex2_approx(fmaf(__uint_as_float(rr[7]), scale_log2, b1.w) - mx);
+          s4[0] += p0 + p4;
+          s4[1] += p1 + p5;
+          s4[2] += p2 + p6;
+          s4[3] += p3 + p7;
+          sts_u4(s_prow + ((chunk ^ (i & 7)) << 4),
+                 make_uint4(pack_bf16(p0, p1), pack_bf16(p2, p3), pack_bf16(p4, p5), pack_bf16(p6, p7)));
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();  // S reads done before the PV MMA may overwrite block 0
+        mbar_arrive(&p_full[g]);
+      }
+      sts_f32(s_red + (256 + g * 128 + i) * 4, (s4[0] + s4[1]) + (s4[2] + s4[3]));
+      named_bar_sync(1, 256);
+      return rcp_approx(lds_f32(s_red + (256 + i) * 4) + lds_f32(s_red + (384 + i) * 4));
+    };
+
+    auto epilogue = [&](uint32_t tcnt, int row_base, int h, int qt, float inv) {
+      const int ss = tcnt % L.n_s;
+      mbar_wait(&o_full[ss], (tcnt / L.n_s) & 1);
+      tc_fence_after();
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(lane_base + ss * 256 + g * 32, o);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&s_free[ss]);
+      const int q = qt * kQTile + i;
+      if (q < t) {
+        uint4* orow = reinterpret_cast<uint4*>(out + (static_cast<long long>(row_base) + q) * D +
+                                               h * kHd + g * 32);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          orow[c] = make_uint4(
+              pack_bf16(__uint_as_float(o[8 * c]) * inv, __uint_as_float(o[8 * c + 1]) * inv),
+              pack_bf16(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv),
+              pack_bf16(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv),
+              pack_bf16(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv));
+      }
+    };
+
+    // deferred epilogue of the previous tile (two-slot mode)
+    bool pend = false;
+    uint32_t pend_t = 0;
+    int pend_row = 0, pend_h = 0, pend_qt = 0;
+    float pend_inv = 0.f;
+    uint32_t tcnt = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int b = item / H, h = item - b * H;
+      const int row_base = b * t;
+      if (pend) {  // bias is rewritten below; the deferred epilogue does not read it
+        epilogue(pend_t, pend_row, pend_h, pend_qt, pend_inv);
+        pend = false;
+      }
+      named_bar_sync(1, 256);  // everyone is done with the previous item's bias
+      for (int j = threadIdx.x; j < L.t_pad; j += 256) {
+        float v = -INFINITY;
+        if (j < t) v = size != nullptr ? __log2f(size[static_cast<long long>(row_base) + j]) : 0.f;
+        bias[j] = v;
+      }
+      named_bar_sync(1, 256);
+      for (int qt = 0; qt < L.n_qt; ++qt, ++tcnt) {
+        const float mx = pass1(tcnt);
+        if (pend) {
+          epilogue(pend_t, pend_row, pend_h, pend_qt, pend_inv);
+          pend = false;
+        }
+        const float inv = pass2(tcnt, mx);
+        if (L.n_s == 2) {
+          pend = true;
+          pend_t = tcnt;
+          pend_row = row_base;
+          pend_h = h;
+          pend_qt = qt;
+          pend_inv = inv;
+        } else {
+          epilogue(tcnt, row_base, h, qt, inv);
+        }
+      }
+    }
+    if (pend) epilogue(pend_t, pend_row, pend_h, pend_qt, pend_inv);
+  }
+  grid_dep_launch();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+// Returns TA_ERR_SHAPE when the shape is outside the tcgen05 kernel's envelope
+// (hd != 64 or t > 512); the caller then uses the mma.sync kernel.
+int attention_tc(const void* qkv, const float* size, int B, int t, int H, int hd, void* out,
+                 cudaStream_t s) {
+  if (hd != kHd || t <= 0 || t > kMaxTPad) return TA_ERR_SHAPE;
+  const AttnTcLayout L = attn_layout(t);
+  CUtensorMap tm;
+  int rc = make_tmap_bf16_2d(&tm, qkv, static_cast<uint64_t>(B) * t, 3ull * H * hd, 64);
+  if (rc) return rc;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
+    if (e != cudaSuccess) return set_last_cuda_error(e);
+    attr_set = true;
+  }
+  const int n_items = B * H;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_items < device_sm_count() ? n_items : device_sm_count());
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = L.smem_bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const float scale_log2 = 1.4426950408889634f / 8.0f;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, attn_tc_kernel, tm, size, t, H, n_items,
+                                     static_cast<__nv_bfloat16*>(out), scale_log2, L);
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
+}  // namespace ta

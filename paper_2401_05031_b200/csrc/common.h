@@ -65,13 +65,20 @@ int head(const float* x, int B, int t_total, int D, const float* nw, const float
 
 // tome.cu.  metric source: either fp32 [B, t, c] (metric != null) or the k third of a
 // qkv activation [B, t, 3*H*c] in `qkv_dtype`, averaged over heads (ToMe k.mean(1)).
+// scratch (nullable): match_tc_scratch_bytes(B, c) bytes; with it the tcgen05 path runs
+// (TA_MATCH_BACKEND=simt forces the SIMT kernel), without it the SIMT kernel.
 int match(const float* metric, const void* qkv, int qkv_dtype, int B, int t, int heads, int c,
-          int r, int32_t* src, int32_t* dst, int32_t* unm, cudaStream_t s);
+          int r, int32_t* src, int32_t* dst, int32_t* unm, float* scratch, cudaStream_t s);
+size_t match_tc_scratch_bytes(int B, int c);
+int match_tc(const float* metric, const void* qkv, int qkv_dtype, int B, int t, int heads, int c,
+             int r, int32_t* src, int32_t* dst, int32_t* unm, float* scratch, cudaStream_t s);
 int merge(const float* x, const float* size, int B, int t, int D, int r, const int32_t* src,
           const int32_t* dst, const int32_t* unm, const float* ln_w, const float* ln_b,
           float* x_out, float* size_out, void* h_out, int h_dtype, cudaStream_t s);
 
-// attention.cu
+// attention.cu / attention_tc.cu
+int attention_tc(const void* qkv, const float* size, int B, int t, int H, int hd, void* out,
+                 cudaStream_t s);
 int attention(const void* qkv, const float* size, int B, int t, int H, int hd, void* out,
               int dtype, cudaStream_t s);
 

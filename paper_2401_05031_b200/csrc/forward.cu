@@ -107,6 +107,7 @@ struct Workspace {
   int32_t* src;
   int32_t* dst;
   int32_t* unm;
+  float* match_scratch;
   size_t total;
 };
 
@@ -132,6 +133,7 @@ Workspace carve(const ta_model* m, int B, const Schedule& s, char* base) {
   w.src = reinterpret_cast<int32_t*>(take(rows * 4));
   w.dst = reinterpret_cast<int32_t*>(take(rows * 4));
   w.unm = reinterpret_cast<int32_t*>(take(rows * 4));
+  w.match_scratch = reinterpret_cast<float*>(take(match_tc_scratch_bytes(B, m->hd)));
   w.total = off;
   return w;
 }
@@ -371,7 +373,8 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
       }
       trace_off += static_cast<size_t>(B) * (2 * r + na - r);
       if (!forced_trace)
-        TA_TRY(match(nullptr, w.qkv, act, B, t, d.heads, m->hd, r, src, dst, unm, st));
+        TA_TRY(match(nullptr, w.qkv, act, B, t, d.heads, m->hd, r, src, dst, unm, w.match_scratch,
+                     st));
       else if (merge_trace)
         cudaMemcpyAsync(merge_trace + (src - forced_trace), src,
                         sizeof(int32_t) * static_cast<size_t>(B) * (2 * r + na - r),
@@ -467,8 +470,15 @@ int ta_forward_host(ta_model* m, const float* images_host, const int32_t* task_i
 int ta_match(const float* metric, int batch, int t, int c, int r, int32_t* src, int32_t* dst,
              int32_t* unm, void* stream) {
   if (!metric || !src || !dst || !unm || batch <= 0) return TA_ERR_INVALID;
-  return match(metric, nullptr, TA_DTYPE_F32, batch, t, 1, c, r, src, dst, unm,
-               static_cast<cudaStream_t>(stream));
+  // Unit entry point (parity tests): scratch for the tcgen05 path is stream-ordered.
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  void* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(&scratch, match_tc_scratch_bytes(batch, c), st);
+  if (e != cudaSuccess) return set_last_cuda_error(e);
+  const int rc = match(metric, nullptr, TA_DTYPE_F32, batch, t, 1, c, r, src, dst, unm,
+                       static_cast<float*>(scratch), st);
+  cudaFreeAsync(scratch, st);
+  return rc;
 }
 
 int ta_merge(const float* x, const float* size, int batch, int t, int dim, int r,

@@ -10,6 +10,7 @@
 // The per-image problem is small (A 99 x B 98 x 64 at t = 197) and latency-bound, so one
 // CTA owns one image; the merge is HBM-bound (read t x D, write t' x D fp32 + t' x D act).
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.h"
 #include "ptx.cuh"
@@ -123,10 +124,23 @@ __global__ void __launch_bounds__(kMatchThreads)
   grid_dep_launch();
 }
 
+static int match_backend() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* v = getenv("TA_MATCH_BACKEND");
+    mode = (v && v[0] == 's') ? 1 : 0;
+  }
+  return mode;
+}
+
 int match(const float* metric, const void* qkv, int qkv_dtype, int B, int t, int heads, int c,
-          int r, int32_t* src, int32_t* dst, int32_t* unm, cudaStream_t s) {
+          int r, int32_t* src, int32_t* dst, int32_t* unm, float* scratch, cudaStream_t s) {
   const int na = (t + 1) / 2, nb = t / 2;
   if (r <= 0 || r > na - 1 || t < 3) return TA_ERR_INVALID;
+  if (scratch != nullptr && match_backend() == 0) {
+    const int rc = match_tc(metric, qkv, qkv_dtype, B, t, heads, c, r, src, dst, unm, scratch, s);
+    if (rc != TA_ERR_SHAPE) return rc;
+  }
   const size_t smem = (static_cast<size_t>(na + nb) * (c + 1) + 3 * na) * sizeof(float);
   if (smem > 220 * 1024) return TA_ERR_SHAPE;
   cudaLaunchConfig_t cfg = {};

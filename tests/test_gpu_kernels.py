@@ -103,7 +103,7 @@ def _attn_ref(qkv, size, b, t, heads, hd):
     return (s.softmax(-1) @ v).transpose(1, 2).reshape(b, t, heads * hd)
 
 
-@pytest.mark.parametrize("t", [1, 17, 64, 101, 197, 389])
+@pytest.mark.parametrize("t", [1, 17, 64, 101, 128, 129, 197, 256, 257, 389, 512, 581])
 @pytest.mark.parametrize("hd,heads", [(64, 12), (80, 16)])
 @pytest.mark.parametrize("with_size", [False, True])
 @pytest.mark.parametrize("dtype", [0, 1])
