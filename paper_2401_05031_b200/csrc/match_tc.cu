@@ -31,7 +31,9 @@ __device__ __forceinline__ float tf32_trunc(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
-// grid (B), block 256.  One warp per token row.
+// grid (B, 8), block 256: one warp per token row, 32 rows per CTA.  Each lane owns column
+// pairs (2 lane, 2 lane + 1) (+64): all heads' k values are loaded before the sum, in head
+// order, so the fixed summation order of the SIMT kernel is kept.
 template <typename QT>
 __global__ void __launch_bounds__(256)
     metric_split_kernel(const float* __restrict__ metric, const QT* __restrict__ qkv, int t,
@@ -41,42 +43,66 @@ __global__ void __launch_bounds__(256)
   float* base = scratch + static_cast<long long>(b) * 4 * kRows * cp;
   grid_dep_wait();
   const int lane = lane_id();
-  for (int row = warp_id(); row < 2 * kRows; row += blockDim.x / 32) {
-    const int set = row / kRows;  // 0 = A (even tokens), 1 = B (odd tokens)
-    const int ri = row % kRows;
+  const int row = blockIdx.y * 32 + warp_id() * 4;
+  for (int rr = row; rr < row + 4; ++rr) {
+    const int set = rr / kRows;  // 0 = A (even tokens), 1 = B (odd tokens)
+    const int ri = rr % kRows;
     const int tok = 2 * ri + set;
     const bool valid = ri < (set ? nb : na);
     float* hi = base + (static_cast<long long>(set * 2) * kRows + ri) * cp;
     float* lo = hi + static_cast<long long>(kRows) * cp;
-    float v[3];  // c <= 96
+    float v[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
     float ss = 0.f;
 #pragma unroll
-    for (int u = 0; u < 3; ++u) {
-      const int j = lane + 32 * u;
-      float x = 0.f;
+    for (int u = 0; u < 2; ++u) {
+      const int j = 2 * lane + 64 * u;  // columns j, j + 1 (c is even)
       if (valid && j < c) {
         if (metric != nullptr) {
-          x = metric[(static_cast<long long>(b) * t + tok) * c + j];
+          const float2 m2 = *reinterpret_cast<const float2*>(
+              metric + (static_cast<long long>(b) * t + tok) * c + j);
+          v[u][0] = m2.x;
+          v[u][1] = m2.y;
         } else {
           const long long D = static_cast<long long>(heads) * c;
           const QT* kr = qkv + (static_cast<long long>(b) * t + tok) * 3 * D + D + j;
-          float acc = 0.f;
-          for (int h = 0; h < heads; ++h) acc += static_cast<float>(kr[h * c]);
-          x = acc / heads;
+          float2 kv[16];
+#pragma unroll
+          for (int h = 0; h < 16; ++h) {
+            if (h < heads) {
+              if constexpr (sizeof(QT) == 2)
+                kv[h] = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(kr + h * c));
+              else
+                kv[h] = *reinterpret_cast<const float2*>(kr + h * c);
+            }
+          }
+          float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+          for (int h = 0; h < 16; ++h) {
+            if (h < heads) {
+              a0 += kv[h].x;
+              a1 += kv[h].y;
+            }
+          }
+          v[u][0] = a0 / heads;
+          v[u][1] = a1 / heads;
         }
       }
-      v[u] = x;
-      ss += x * x;
+      ss += v[u][0] * v[u][0] + v[u][1] * v[u][1];
     }
     const float nrm = sqrtf(warp_sum(ss));
 #pragma unroll
-    for (int u = 0; u < 3; ++u) {
-      const int j = lane + 32 * u;
+    for (int u = 0; u < 2; ++u) {
+      const int j = 2 * lane + 64 * u;
       if (j < cp) {
-        const float x = valid ? v[u] / nrm : 0.f;
-        const float h = tf32_trunc(x);
-        hi[j] = h;
-        lo[j] = tf32_trunc(x - h);
+        float2 h2, l2;
+        const float x0 = valid ? v[u][0] / nrm : 0.f;
+        const float x1 = valid ? v[u][1] / nrm : 0.f;
+        h2.x = tf32_trunc(x0);
+        h2.y = tf32_trunc(x1);
+        l2.x = tf32_trunc(x0 - h2.x);
+        l2.y = tf32_trunc(x1 - h2.y);
+        *reinterpret_cast<float2*>(hi + j) = h2;
+        *reinterpret_cast<float2*>(lo + j) = l2;
       }
     }
   }
@@ -246,14 +272,14 @@ int match_tc(const float* metric, const void* qkv, int qkv_dtype, int B, int t, 
              int r, int32_t* src, int32_t* dst, int32_t* unm, float* scratch, cudaStream_t s) {
   const int na = (t + 1) / 2;
   if (r <= 0 || r > na - 1 || t < 3) return TA_ERR_INVALID;
-  if (t > 2 * kRows || c > 96 || scratch == nullptr) return TA_ERR_SHAPE;
+  if (t > 2 * kRows || c > 96 || (c & 1) || heads > 16 || scratch == nullptr) return TA_ERR_SHAPE;
   const int cp = (c + 31) / 32 * 32;
   cudaError_t e;
   if (metric != nullptr || qkv_dtype == TA_DTYPE_F32)
-    e = launch_pdl(metric_split_kernel<float>, dim3(B), dim3(256), 0, s, metric,
+    e = launch_pdl(metric_split_kernel<float>, dim3(B, 2 * kRows / 32), dim3(256), 0, s, metric,
                    static_cast<const float*>(qkv), t, heads, c, cp, scratch);
   else
-    e = launch_pdl(metric_split_kernel<__nv_bfloat16>, dim3(B), dim3(256), 0, s, metric,
+    e = launch_pdl(metric_split_kernel<__nv_bfloat16>, dim3(B, 2 * kRows / 32), dim3(256), 0, s, metric,
                    static_cast<const __nv_bfloat16*>(qkv), t, heads, c, cp, scratch);
   if (e != cudaSuccess) return set_last_cuda_error(e);
   CUtensorMap tm;
