@@ -13,6 +13,7 @@
 // fp32 path: SIMT FFMA tile kernel with the same epilogues, used by the fp32 parity
 // mode (north_star: merge index sets bit-exact in fp32 mode).
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include <cudaTypedefs.h>
@@ -304,6 +305,193 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------ tcgen05 CTA-pair kernel
+// Cluster of 2 CTAs on one TPC computes a 256 x 256 tile with tcgen05.mma.cta_group::2:
+// each CTA stages its 128 rows of A and its 128-row half of W per K block (32 KB), so L2 ->
+// SM operand traffic per FLOP is 2/3 of the single-CTA 128 x 256 kernel and each SM's tensor
+// core reads half of B from the peer's smem.  The leader (rank 0) issues all MMAs; its
+// commits multicast to both CTAs' barriers; each CTA's epilogue drains its own 128 TMEM
+// lanes and releases the accumulator to the leader with a cluster-scope arrive.
+constexpr int kPairStages = 6;
+struct PairCfg {
+  static constexpr int kABytes = 128 * kBK * 2;
+  static constexpr int kBBytes = 128 * kBK * 2;  // this CTA's half of the 256-row W tile
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kEpiBytes = kEpiWarps * 32 * 32 * 4;
+  static constexpr int kSmemBytes = kPairStages * kStageBytes + kEpiBytes + 1024 + 256;
+};
+
+template <int EPI, typename OutT, bool kRemap>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    gemm_bf16_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                                const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                                GemmEpi epi) {
+  constexpr int BN = 256;
+  constexpr int S = kPairStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  float4* epi_stage = reinterpret_cast<float4*>(smem + S * PairCfg::kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * PairCfg::kStageBytes + PairCfg::kEpiBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * 32 * kEpiWarps);  // both CTAs' epilogue threads (leader's copy)
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  grid_dep_wait();
+
+  const int num_m = (M + 255) / 256;
+  const int num_n = N / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = K / kBK;
+  const int cid = static_cast<int>(cluster_id_x());
+  const int ncl = static_cast<int>(nclusters_x());
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full_leader0 = mapa_shared(&full[0], 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
+        const int m_blk = tile / num_n;
+        const int n_blk = tile - m_blk * num_n;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * PairCfg::kStageBytes;
+          uint8_t* sb = sa + PairCfg::kABytes;
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * PairCfg::kStageBytes);
+          const uint32_t fb = full_leader0 + stage * 8;
+          tma_load_2d_pair(&tmA, fb, sa, kb * kBK, m_blk * 256 + rank * 128);
+          tma_load_2d_pair(&tmB, fb, sb, kb * kBK, n_blk * BN + rank * 128);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(256, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
+        mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * PairCfg::kStageBytes);
+          const uint32_t sb = sa + PairCfg::kABytes;
+          const uint64_t adesc = umma_desc_sw128(sa);
+          const uint64_t bdesc = umma_desc_sw128(sb);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            umma_f16_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          umma_commit_pair(&empty[stage]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t ew = warp - 4;
+    const uint32_t q = ew & 3;
+    const int col0 = (ew >> 2) * (BN / 2);
+    constexpr int kChunks = BN / 2 / 32;
+    float4* stage = epi_stage + ew * 256;
+    const uint32_t tempty_leader0 = mapa_shared(&tempty[0], 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = cid; tile < num_tiles; tile += ncl) {
+      const int m_blk = tile / num_n;
+      const int n_blk = tile - m_blk * num_n;
+      const long long m_base = static_cast<long long>(m_blk) * 256 + rank * 128 + q * 32;
+      if constexpr (EPI == EPI_BIAS_RESID) {
+        const long long m = m_base + lane;
+        if (m < M)
+          prefetch_l2_bulk(epi.resid + m * N + n_blk * BN + col0, BN / 2 * sizeof(float));
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * BN + col0;
+      uint32_t r0[32], r1[32];
+      EpiChunk ca, cb;
+      const bool live = m_base < M;
+      const int nb = n_blk * BN + col0;
+      tmem_ld_32x32b_x32(t_row, r0);
+      tmem_ld_wait();
+      if (live) epi_load<EPI>(epi, M, N, m_base, nb, r0, stage, ca);
+#pragma unroll 1
+      for (int c = 0; c < kChunks; c += 2) {
+        tmem_ld_32x32b_x32(t_row + (c + 1) * 32, r1);
+        tmem_ld_wait();
+        if (c + 2 == kChunks) {
+          tc_fence_before();
+          mbar_arrive_remote(tempty_leader0 + acc * 8);
+        }
+        if (live) {
+          epi_load<EPI>(epi, M, N, m_base, nb + (c + 1) * 32, r1, stage, cb);
+          epi_store<EPI, OutT, kRemap>(epi, M, N, m_base, nb + c * 32, ca);
+        }
+        if (c + 2 < kChunks) {
+          tmem_ld_32x32b_x32(t_row + (c + 2) * 32, r0);
+          tmem_ld_wait();
+          if (live) epi_load<EPI>(epi, M, N, m_base, nb + (c + 2) * 32, r0, stage, ca);
+        }
+        if (live) epi_store<EPI, OutT, kRemap>(epi, M, N, m_base, nb + (c + 1) * 32, cb);
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  grid_dep_launch();
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair<512>(tmem_base);
+  }
+}
+
 // ------------------------------------------------------------------ SIMT fp32 kernel
 // 128 x 128 tile, BK = 8, 256 threads, 8 x 8 outputs per thread.  fp32 FFMA only:
 // products are exact fp32 so results differ from a CPU fp32 GEMM by summation order.
@@ -433,6 +621,61 @@ static int launch_bf16(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 
+template <int EPI, typename OutT, bool kRemap = false>
+static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, int N, int K,
+                       const GemmEpi& epi, cudaStream_t stream) {
+  auto kern = gemm_bf16_sm100_pair_kernel<EPI, OutT, kRemap>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         PairCfg::kSmemBytes);
+    if (e != cudaSuccess) return set_last_cuda_error(e);
+    attr_set = true;
+  }
+  const int tiles = ((M + 255) / 256) * (N / 256);
+  const int pairs = device_sm_count() / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * (tiles < pairs ? tiles : pairs));
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = PairCfg::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta_, tb_, M, N, K, epi);
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
+static int dispatch_pair(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
+                         int epi_kind, bool out_bf16, const GemmEpi& epi, cudaStream_t s) {
+  switch (epi_kind) {
+    case EPI_BIAS:
+      return out_bf16 ? launch_pair<EPI_BIAS, __nv_bfloat16>(a, b, M, N, K, epi, s)
+                      : launch_pair<EPI_BIAS, float>(a, b, M, N, K, epi, s);
+    case EPI_BIAS_GELU:
+      return out_bf16 ? launch_pair<EPI_BIAS_GELU, __nv_bfloat16>(a, b, M, N, K, epi, s)
+                      : launch_pair<EPI_BIAS_GELU, float>(a, b, M, N, K, epi, s);
+    case EPI_BIAS_RESID:
+      return epi.rows_in ? launch_pair<EPI_BIAS_RESID, float, true>(a, b, M, N, K, epi, s)
+                         : launch_pair<EPI_BIAS_RESID, float, false>(a, b, M, N, K, epi, s);
+    case EPI_PATCH:
+      return launch_pair<EPI_PATCH, float, true>(a, b, M, N, K, epi, s);
+  }
+  return TA_ERR_INVALID;
+}
+
+// 0 = CTA-pair kernel where it applies (default), 1 = single-CTA kernel (TA_GEMM_BACKEND=single).
+static int gemm_backend() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* v = getenv("TA_GEMM_BACKEND");
+    mode = (v && v[0] == 's') ? 1 : 0;
+  }
+  return mode;
+}
+
 template <int BN>
 static int dispatch_bf16(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
                          int epi_kind, bool out_bf16, const GemmEpi& epi, cudaStream_t s) {
@@ -461,6 +704,11 @@ int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, b
   CUtensorMap ta_, tb_;
   int rc = make_tmap_bf16_2d(&ta_, A, M, K, kBM);
   if (rc) return rc;
+  if (BN == 256 && gemm_backend() == 0) {
+    rc = make_tmap_bf16_2d(&tb_, W, N, K, 128);  // each CTA of the pair loads 128 W rows
+    if (rc) return rc;
+    return dispatch_pair(ta_, tb_, M, N, K, epi_kind, out_bf16, epi, stream);
+  }
   rc = make_tmap_bf16_2d(&tb_, W, N, K, BN);
   if (rc) return rc;
   return BN == 256 ? dispatch_bf16<256>(ta_, tb_, M, N, K, epi_kind, out_bf16, epi, stream)
