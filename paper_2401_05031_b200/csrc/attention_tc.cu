@@ -10,8 +10,9 @@
 //                    softmax warps never wait for it; O += P_blk V_blk per 64-key block with
 //                    V as an MN-major B operand.
 //   warps 0..7       softmax in two groups over even / odd 64-key blocks; query row i is
-//                    TMEM lane i (warps w and w+4 share lanes 32(w%4)..); pass 1 row max of
-//                    s * log2(e)/sqrt(hd) + log2(size_j), pass 2 p = 2^(v - max) -> bf16 P
+//                    TMEM lane i (warps w and w+4 share lanes 32(w%4)..); pass 1 row max m
+//                    of the raw scores, pass 2 p = size_j * 2^((s - m) log2(e)/sqrt(hd))
+//                    (= the log-size bias as a weight; size 0 masks keys >= t) -> bf16 P
 //                    block into ring stage g (SW128, K-major) -> PV MMA; row max / sum
 //                    combined through smem; epilogue O / sum -> bf16 rows.
 // TMEM: slot s at columns [256 s, 256 s + t_pad); O aliases the slot's S block 0, which
@@ -58,11 +59,11 @@ AttnTcLayout attn_layout(int t) {
   L.n_kv = L.t_pad <= 256 ? 2 : 1;
   L.n_s = L.t_pad <= 256 ? 2 : 1;
   L.kv_bytes = 2u * L.n_kb * kBlkBytes;
-  uint32_t off = 2 * kQBytes;  // Q ring
+  uint32_t off = kQBytes;  // Q: one slot (Q(n+1) is only needed after S(n) has long completed)
   L.kv_off = off;
   off += L.n_kv * L.kv_bytes;
   L.p_off = off;
-  off += 2 * kPBytes;
+  off += 4 * kPBytes;  // P ring: two stages per softmax group
   L.bias_off = off;
   off += kMaxTPad * 4;
   L.red_off = off;
@@ -80,6 +81,7 @@ __device__ __forceinline__ void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+template <bool kHasSize>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const float* __restrict__ size, int t,
                    int H, int n_items, __nv_bfloat16* __restrict__ out, float scale_log2,
@@ -101,9 +103,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* s_full = bars + 8;    // [2]
   uint64_t* s_free = bars + 10;   // [2]
   uint64_t* o_full = bars + 12;   // [2]
-  uint64_t* p_full = bars + 14;   // [2]
-  uint64_t* p_free = bars + 16;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* p_full = bars + 14;   // [4]
+  uint64_t* p_free = bars + 18;   // [4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   if (warp == 8 && lane == 0) {
@@ -116,6 +118,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&s_full[s], 1);
       mbar_init(&s_free[s], 256);
       mbar_init(&o_full[s], 1);
+    }
+    for (int s = 0; s < 4; ++s) {
       mbar_init(&p_full[s], 128);
       mbar_init(&p_free[s], 1);
     }
@@ -147,12 +151,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d(&tm, &kv_full[kvs], sV + kb * kBlkBytes, 2 * D + h * kHd, row_base + kb * kKeyBlk);
         }
         for (int qt = 0; qt < L.n_qt; ++qt, ++qcnt) {
-          const int qs = qcnt & 1;
-          mbar_wait(&q_free[qs], ((qcnt >> 1) & 1) ^ 1);
-          mbar_arrive_expect_tx(&q_full[qs], kQBytes);
-          tma_load_2d(&tm, &q_full[qs], sQ + qs * kQBytes, h * kHd, row_base + qt * kQTile);
-          tma_load_2d(&tm, &q_full[qs], sQ + qs * kQBytes + kBlkBytes, h * kHd,
-                      row_base + qt * kQTile + 64);
+          mbar_wait(&q_free[0], (qcnt & 1) ^ 1);
+          mbar_arrive_expect_tx(&q_full[0], kQBytes);
+          tma_load_2d(&tm, &q_full[0], sQ, h * kHd, row_base + qt * kQTile);
+          tma_load_2d(&tm, &q_full[0], sQ + kBlkBytes, h * kHd, row_base + qt * kQTile + 64);
         }
       }
     }
@@ -160,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_pv = idesc_bf16(kQTile, kHd, /*b_mn_major=*/true);
-      uint32_t p_use[2] = {0, 0};
+      uint32_t p_use[2] = {0, 0};  // per softmax group; stage = 2 g + (use & 1)
       // pending PV tile (issued after the next tile's S so softmax never waits)
       int pend_slot = -1, pend_kvs = 0;
       bool pend_last = false;
@@ -168,8 +170,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint8_t* sV = sKV + kvs * L.kv_bytes + L.n_kb * kBlkBytes;
         const uint32_t o_tmem = tmem + sslot * 256;
         for (int kb = 0; kb < L.n_kb; ++kb) {
-          const int ps = kb & 1;
-          mbar_wait(&p_full[ps], p_use[ps]++ & 1);
+          const int grp = kb & 1;
+          const uint32_t u = p_use[grp]++;
+          const int ps = 2 * grp + (u & 1);
+          mbar_wait(&p_full[ps], (u >> 1) & 1);
           tc_fence_after();
           const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
           const uint32_t vbase = smem_u32(sV + kb * kBlkBytes);
@@ -190,17 +194,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t kv_use = it / L.n_kv;
         const uint8_t* sK = sKV + kvs * L.kv_bytes;
         for (int qt = 0; qt < L.n_qt; ++qt, ++qcnt, ++tcnt) {
-          const int qs = qcnt & 1;
           const int ss = tcnt % L.n_s;
           if (L.n_s == 1 && pend_slot >= 0) {  // single S slot: finish the previous tile first
             issue_pv(pend_slot, pend_kvs, pend_last);
             pend_slot = -1;
           }
           mbar_wait(&s_free[ss], ((tcnt / L.n_s) & 1) ^ 1);
-          mbar_wait(&q_full[qs], (qcnt >> 1) & 1);
+          mbar_wait(&q_full[0], qcnt & 1);
           if (qt == 0) mbar_wait(&kv_full[kvs], kv_use & 1);
           tc_fence_after();
-          const uint64_t qdesc = umma_desc_sw128(smem_u32(sQ + qs * kQBytes));
+          const uint64_t qdesc = umma_desc_sw128(smem_u32(sQ));
           for (int n0 = 0; n0 < L.t_pad; n0 += 256) {
             const int n = L.t_pad - n0 < 256 ? L.t_pad - n0 : 256;
             const uint32_t idesc_s = idesc_bf16(kQTile, n);
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               umma_f16(tmem + ss * 256 + n0, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0);
           }
           umma_commit(&s_full[ss]);
-          umma_commit(&q_free[qs]);
+          umma_commit(&q_free[0]);
           if (pend_slot >= 0) issue_pv(pend_slot, pend_kvs, pend_last);
           pend_slot = ss;
           pend_kvs = kvs;
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // shared-space addresses (explicit ld/st.shared; see lds_f4)
     const uint32_t s_bias = smem_u32(bias);
     const uint32_t s_red = smem_u32(red);
-    const uint32_t s_prow = smem_u32(sP) + g * kPBytes + i * 128;
+    const uint32_t s_prow0 = smem_u32(sP) + 2 * g * kPBytes + i * 128;  // + (use & 1) stage
 
     auto pass1 = [&](uint32_t tcnt) -> float {
       const int ss = tcnt % L.n_s;
@@ -244,18 +247,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_32x32b_x32(la + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
         tmem_ld_32x32b_x32(la + kb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
         tmem_ld_wait();
+        if ((kb + 1) * 64 <= t) {
 #pragma unroll
-        for (int j = 0; j < 64; j += 4) {
-          const float4 bb = lds_f4(s_bias + (kb * 64 + j) * 4);
-          m4[0] = fmaxf(m4[0], fmaf(__uint_as_float(r[j]), scale_log2, bb.x));
-          m4[1] = fmaxf(m4[1], fmaf(__uint_as_float(r[j + 1]), scale_log2, bb.y));
-          m4[2] = fmaxf(m4[2], fmaf(__uint_as_float(r[j + 2]), scale_log2, bb.z));
-          m4[3] = fmaxf(m4[3], fmaf(__uint_as_float(r[j + 3]), scale_log2, bb.w));
+          for (int j = 0; j < 64; j += 4) {
+            m4[0] = fmaxf(m4[0], __uint_as_float(r[j]));
+            m4[1] = fmaxf(m4[1], __uint_as_float(r[j + 1]));
+            m4[2] = fmaxf(m4[2], __uint_as_float(r[j + 2]));
+            m4[3] = fmaxf(m4[3], __uint_as_float(r[j + 3]));
+          }
+        } else {  // last block: keys >= t are not part of the row
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (kb * 64 + j < t) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(r[j]));
         }
       }
       sts_f32(s_red + (g * 128 + i) * 4, fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])));
       named_bar_sync(1, 256);
-      return fmaxf(lds_f32(s_red + i * 4), lds_f32(s_red + (128 + i) * 4));
+      // row max of the raw scores, in the scaled log2 domain
+      return fmaxf(lds_f32(s_red + i * 4), lds_f32(s_red + (128 + i) * 4)) * scale_log2;
     };
 
     auto pass2 = [&](uint32_t tcnt, float mx) -> float {
@@ -265,21 +274,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[64];
         tmem_ld_32x32b_x32(la + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
         tmem_ld_32x32b_x32(la + kb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-        mbar_wait(&p_free[g], (use & 1) ^ 1);
+        const int pst = 2 * g + (use & 1);
+        const uint32_t s_prow = s_prow0 + (use & 1) * kPBytes;
+        mbar_wait(&p_free[pst], ((use >> 1) & 1) ^ 1);
         tmem_ld_wait();
+        // p_j = size_j * 2^(s_j * scale - max): the log-size bias as a weight (size 0 masks
+        // keys >= t); without a size vector only the last block needs the mask.
+        const bool weighted = kHasSize || (kb + 1) * 64 > t;
+        const float nmx = -mx;
 #pragma unroll
         for (int chunk = 0; chunk < 8; ++chunk) {  // 8 keys = one 16-byte chunk of the P row
-          const float4 b0 = lds_f4(s_bias + (kb * 64 + chunk * 8) * 4);
-          const float4 b1 = lds_f4(s_bias + (kb * 64 + chunk * 8 + 4) * 4);
           const uint32_t* rr = &r[chunk * 8];
-          const float p0 = ex2_approx(fmaf(__uint_as_float(rr[0]), scale_log2, b0.x) - mx);
-          const float p1 = ex2_approx(fmaf(__uint_as_float(rr[1]), scale_log2, b0.y) - mx);
-          const float p2 = ex2_approx(fmaf(__uint_as_float(rr[2]), scale_log2, b0.z) - mx);
-          const float p3 = ex2_approx(fmaf(__uint_as_float(rr[3]), scale_log2, b0.w) - mx);
-          const float p4 = ex2_approx(fmaf(__uint_as_float(rr[4]), scale_log2, b1.x) - mx);
-          const float p5 = ex2_approx(fmaf(__uint_as_float(rr[5]), scale_log2, b1.y) - mx);
-          const float p6 = ex2_approx(fmaf(__uint_as_float(rr[6]), scale_log2, b1.z) - mx);
-          const float p7 = ex2_approx(fmaf(__uint_as_float(rr[7]), scale_log2, b1.w) - mx);
+          float p0 = ex2_approx(fmaf(__uint_as_float(rr[0]), scale_log2, nmx));
+          float p1 = ex2_approx(fmaf(__uint_as_float(rr[1]), scale_log2, nmx));
+          float p2 = ex2_approx(fmaf(__uint_as_float(rr[2]), scale_log2, nmx));
+          float p3 = ex2_approx(fmaf(__uint_as_float(rr[3]), scale_log2, nmx));
+          float p4 = ex2_approx(fmaf(__uint_as_float(rr[4]), scale_log2, nmx));
+          float p5 = ex2_approx(fmaf(__uint_as_float(rr[5]), scale_log2, nmx));
+          float p6 = ex2_approx(fmaf(__uint_as_float(rr[6]), scale_log2, nmx));
+          float p7 = ex2_approx(fmaf(__uint_as_float(rr[7]), scale_log2, nmx));
+          if (weighted) {
+            const float4 w0 = lds_f4(s_bias + (kb * 64 + chunk * 8) * 4);
+            const float4 w1 = lds_f4(s_bias + (kb * 64 + chunk * 8 + 4) * 4);
+            p0 *= w0.x;
+            p1 *= w0.y;
+            p2 *= w0.z;
+            p3 *= w0.w;
+            p4 *= w1.x;
+            p5 *= w1.y;
+            p6 *= w1.z;
+            p7 *= w1.w;
+          }
           s4[0] += p0 + p4;
           s4[1] += p1 + p5;
           s4[2] += p2 + p6;
@@ -289,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_proxy_async_smem();
         tc_fence_before();  // S reads done before the PV MMA may overwrite block 0
-        mbar_arrive(&p_full[g]);
+        mbar_arrive(&p_full[pst]);
       }
       sts_f32(s_red + (256 + g * 128 + i) * 4, (s4[0] + s4[1]) + (s4[2] + s4[3]));
       named_bar_sync(1, 256);
@@ -325,18 +350,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     int pend_row = 0, pend_h = 0, pend_qt = 0;
     float pend_inv = 0.f;
     uint32_t tcnt = 0;
+    // log2(size) of the item's keys j = threadIdx.x + 256 k (k < 2), loaded one item ahead
+    auto load_bias = [&](int item, float (&v)[2]) {
+      const int row_base_n = (item / H) * t;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int j = threadIdx.x + 256 * k;
+        v[k] = (j < t && size != nullptr) ? size[static_cast<long long>(row_base_n) + j] : 1.f;
+      }
+    };
+    float sz_next[2];
+    if (blockIdx.x < n_items) load_bias(blockIdx.x, sz_next);
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int b = item / H, h = item - b * H;
       const int row_base = b * t;
+      float sz[2] = {sz_next[0], sz_next[1]};
+      if (item + static_cast<int>(gridDim.x) < n_items) load_bias(item + gridDim.x, sz_next);
       if (pend) {  // bias is rewritten below; the deferred epilogue does not read it
         epilogue(pend_t, pend_row, pend_h, pend_qt, pend_inv);
         pend = false;
       }
       named_bar_sync(1, 256);  // everyone is done with the previous item's bias
-      for (int j = threadIdx.x; j < L.t_pad; j += 256) {
-        float v = -INFINITY;
-        if (j < t) v = size != nullptr ? __log2f(size[static_cast<long long>(row_base) + j]) : 0.f;
-        bias[j] = v;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int j = threadIdx.x + 256 * k;
+        if (j < L.t_pad) sts_f32(s_bias + j * 4, j < t ? sz[k] : 0.f);  // key weight
       }
       named_bar_sync(1, 256);
       for (int qt = 0; qt < L.n_qt; ++qt, ++tcnt) {
@@ -382,8 +420,11 @@ int attention_tc(const void* qkv, const float* size, int B, int t, int H, int hd
   if (rc) return rc;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               227 * 1024);
     if (e != cudaSuccess) return set_last_cuda_error(e);
     attr_set = true;
   }
@@ -399,8 +440,10 @@ int attention_tc(const void* qkv, const float* size, int B, int t, int H, int hd
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const float scale_log2 = 1.4426950408889634f / 8.0f;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, attn_tc_kernel, tm, size, t, H, n_items,
-                                     static_cast<__nv_bfloat16*>(out), scale_log2, L);
+  auto* o = static_cast<__nv_bfloat16*>(out);
+  cudaError_t e = size != nullptr
+                      ? cudaLaunchKernelEx(&cfg, attn_tc_kernel<true>, tm, size, t, H, n_items, o, scale_log2, L)
+                      : cudaLaunchKernelEx(&cfg, attn_tc_kernel<false>, tm, size, t, H, n_items, o, scale_log2, L);
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 
