@@ -228,13 +228,12 @@ def run_ours(args):
             ms = evs[i].elapsed_time(evs[i + 1])
             per_gamma_ms[g] += ms
             total_ms += ms
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-        dist.barrier()
+    from paper_2401_05031_b200.replicas import aggregate_throughput
 
-    imgs_total = args.steps * len(gammas) * B * world
+    # replicas only: images summed over ranks, device time = max over ranks
+    imgs_total, total_ms = aggregate_throughput(args.steps * len(gammas) * B, total_ms)
+    if world > 1:
+        dist.barrier()
     value = imgs_total / (total_ms / 1e3)
     peak, peak_sus, hbm, peak_src = _peaks()
     flops = {g: flops_per_image(cfg, g) for g in gammas}
