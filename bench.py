@@ -175,7 +175,7 @@ def run_ours(args):
     cfg, params = helpers.backbone(args.model)
     gammas = GAMMAS
     tasks = helpers.task_params(cfg, (100,), [g for g in gammas if g > 0])
-    sm = helpers.serve_model(cfg, params, tasks, dtype="bf16")
+    sm = helpers.serve_model(cfg, params, tasks, dtype="bf16", fold_ln=bool(args.fold_ln))
     bb = sm.backbone
     B = args.batch
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -350,6 +350,7 @@ def main():
     ap.add_argument("--cpu-batch", type=int, default=8)
     ap.add_argument("--ref-batch", type=int, default=4)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--fold-ln", type=int, default=0, help="fold LayerNorm into the QKV / fc1 GEMMs")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

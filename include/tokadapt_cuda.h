@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define TA_ABI_VERSION 1
+#define TA_ABI_VERSION 2
 
 /* Status codes.  Python maps them onto the reference's exception types
  * (pkg/src/tokadapt/errors.py): TA_ERR_NO_PROMPT -> ProfileGapError(task, gamma,
@@ -92,6 +92,19 @@ typedef struct ta_layer_weights {
   const void* fc1_b;
   const void* fc2_w; /* [D, MLP] */
   const void* fc2_b;
+  /* Optional (bf16 mode; all six or none): LayerNorm folded into the QKV / fc1 GEMMs.
+   *   *_w_ln = bf16(W o gamma)  [out, in]     (gamma = ln1_w for QKV, ln2_w for fc1)
+   *   *_c1   = fp32 row sums of *_w_ln [out]
+   *   *_c2   = fp32 W beta + b [out]          (beta = ln1_b / ln2_b)
+   * With them ta_forward drops the LayerNorm passes: the residual's producers also emit a
+   * bf16 copy and per-row (sum, sumsq), and the GEMM epilogue finishes
+   * LN(x) W^T + b = rstd (x W_ln^T - mu c1) + c2. */
+  const void* qkv_w_ln;
+  const void* qkv_c1;
+  const void* qkv_c2;
+  const void* fc1_w_ln;
+  const void* fc1_c1;
+  const void* fc1_c2;
 } ta_layer_weights;
 
 typedef struct ta_weights {

@@ -47,7 +47,8 @@ class ModelDesc(ctypes.Structure):
 class LayerWeights(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in (
         "ln1_w", "ln1_b", "qkv_w", "qkv_b", "proj_w", "proj_b", "ln2_w", "ln2_b",
-        "fc1_w", "fc1_b", "fc2_w", "fc2_b")]
+        "fc1_w", "fc1_b", "fc2_w", "fc2_b",
+        "qkv_w_ln", "qkv_c1", "qkv_c2", "fc1_w_ln", "fc1_c1", "fc1_c2")]
 
 
 class Weights(ctypes.Structure):

@@ -15,7 +15,26 @@ enum EpiKind : int {
   EPI_BIAS_GELU = 1,   // out(act dtype) = gelu_erf(acc + bias)
   EPI_BIAS_RESID = 2,  // out(fp32)      = resid[m] + acc + bias   (residual stream update)
   EPI_PATCH = 3,       // out(fp32)      = acc + bias + pos[row]   (patch embedding)
+  // LayerNorm folded into the next GEMM (bf16 path).  Producers also write xh = bf16(out)
+  // and accumulate per-row (sum, sum of squares) of out into stats[out_row] (atomics):
+  EPI_BIAS_RESID_STATS = 4,
+  EPI_PATCH_STATS = 5,
+  // Consumers take A = xh and W' = W o gamma and finish LN(x) W^T + b exactly as
+  //   out = rstd * (acc - mu * c1[n]) + c2[n],  c1 = rowsum(W'), c2 = W beta + b,
+  // with mu / rstd from ln_stats[m] (eps 1e-6, biased variance):
+  EPI_LN_BIAS = 6,     // out(bf16) = LN(x) W^T + b        (QKV)
+  EPI_LN_GELU = 7,     // out(bf16) = gelu(LN(x) W^T + b)  (fc1)
 };
+
+__host__ __device__ constexpr bool epi_is_stats(int e) {
+  return e == EPI_BIAS_RESID_STATS || e == EPI_PATCH_STATS;
+}
+__host__ __device__ constexpr bool epi_is_ln(int e) { return e == EPI_LN_BIAS || e == EPI_LN_GELU; }
+__host__ __device__ constexpr bool epi_is_resid(int e) {
+  return e == EPI_BIAS_RESID || e == EPI_BIAS_RESID_STATS;
+}
+__host__ __device__ constexpr bool epi_is_patch(int e) { return e == EPI_PATCH || e == EPI_PATCH_STATS; }
+__host__ __device__ constexpr bool epi_is_gelu(int e) { return e == EPI_BIAS_GELU || e == EPI_LN_GELU; }
 
 struct GemmEpi {
   const float* bias = nullptr;   // [N]
@@ -28,6 +47,14 @@ struct GemmEpi {
   int rows_in = 0;
   int rows_out = 0;
   int row_off = 0;
+  // LayerNorm folding (EPI_*_STATS producers / EPI_LN_* consumers)
+  void* xh = nullptr;               // producer: bf16 copy of out, same rows
+  float* stats = nullptr;           // producer: [rows, 2] (sum, sumsq), pre-zeroed, atomics
+  const float* ln_stats = nullptr;  // consumer: [M, 2] stats of the A rows
+  const float* c1 = nullptr;        // consumer: [N]
+  const float* c2 = nullptr;        // consumer: [N]
+  float inv_dim = 0.f;              // consumer: 1 / D
+  int skip = 0;                     // profiling only (TA_GEMM_SKIP_EPILOGUE=1): no epilogue work
 };
 
 __host__ __device__ inline long long epi_out_row(const GemmEpi& e, long long m) {
@@ -57,7 +84,7 @@ int gemm_f32(const float* A, const float* W, int M, int N, int K, int epi_kind,
 int patchify(const float* img, void* out, int B, int S, int P, int Kp, int dtype, cudaStream_t s);
 int insert_rows(float* x, int B, int t_total, int D, const float* cls, const float* pos,
                 const float* const* prompt_tab, const int32_t* task_ids, int layer, int gamma,
-                int prompt_row, cudaStream_t s);
+                int prompt_row, cudaStream_t s, void* xh = nullptr, float* stats = nullptr);
 int layernorm(const float* x, const float* w, const float* b, void* out, int rows, int D,
               int out_dtype, cudaStream_t s);
 int head(const float* x, int B, int t_total, int D, const float* nw, const float* nb,
@@ -74,7 +101,8 @@ int match_tc(const float* metric, const void* qkv, int qkv_dtype, int B, int t, 
              int r, int32_t* src, int32_t* dst, int32_t* unm, float* scratch, cudaStream_t s);
 int merge(const float* x, const float* size, int B, int t, int D, int r, const int32_t* src,
           const int32_t* dst, const int32_t* unm, const float* ln_w, const float* ln_b,
-          float* x_out, float* size_out, void* h_out, int h_dtype, cudaStream_t s);
+          float* x_out, float* size_out, void* h_out, int h_dtype, cudaStream_t s,
+          float* stats_out = nullptr);  // stats_out: write bf16(x') + row (sum, sumsq) instead of LN2
 
 // attention.cu / attention_tc.cu
 int attention_tc(const void* qkv, const float* size, int B, int t, int H, int hd, void* out,

@@ -53,6 +53,7 @@ struct ta_model {
   ta_model_desc d{};
   int hd = 0, grid = 0, n_patches = 0, n_tokens = 0, kp = 0;
   bool has_weights = false;
+  bool ln_folded = false;  // every layer has the LN-folded QKV / fc1 weights
   ta_weights w{};
   std::vector<ta_layer_weights> layers;
   std::vector<HeadDesc> heads;  // host copy
@@ -108,6 +109,7 @@ struct Workspace {
   int32_t* dst;
   int32_t* unm;
   float* match_scratch;
+  float* stats[2];  // LN-folded path: per-row (sum, sumsq) for LN1 / LN2
   size_t total;
 };
 
@@ -134,6 +136,8 @@ Workspace carve(const ta_model* m, int B, const Schedule& s, char* base) {
   w.dst = reinterpret_cast<int32_t*>(take(rows * 4));
   w.unm = reinterpret_cast<int32_t*>(take(rows * 4));
   w.match_scratch = reinterpret_cast<float*>(take(match_tc_scratch_bytes(B, m->hd)));
+  w.stats[0] = reinterpret_cast<float*>(take(rows * 8));
+  w.stats[1] = reinterpret_cast<float*>(take(rows * 8));
   w.total = off;
   return w;
 }
@@ -141,7 +145,7 @@ Workspace carve(const ta_model* m, int B, const Schedule& s, char* base) {
 int linear(const ta_model* m, const void* a, const void* wt, int M, int N, int K, int epi_kind,
            const GemmEpi& epi, cudaStream_t st) {
   if (m->d.dtype == TA_DTYPE_BF16)
-    return gemm_bf16(a, wt, M, N, K, epi_kind, epi_kind == EPI_BIAS || epi_kind == EPI_BIAS_GELU,
+    return gemm_bf16(a, wt, M, N, K, epi_kind, epi_kind == EPI_BIAS || epi_kind == EPI_BIAS_GELU || epi_is_ln(epi_kind),
                      epi, st);
   return gemm_f32(static_cast<const float*>(a), static_cast<const float*>(wt), M, N, K, epi_kind,
                   epi, st);
@@ -238,6 +242,12 @@ int ta_model_set_weights(ta_model* m, const ta_weights* w) {
   }
   m->w = *w;
   m->layers.assign(w->layers, w->layers + m->d.depth);
+  bool folded = true;
+  for (const ta_layer_weights& L : m->layers)
+    folded = folded && L.qkv_w_ln && L.qkv_c1 && L.qkv_c2 && L.fc1_w_ln && L.fc1_c1 && L.fc1_c2;
+  // the folded epilogues exist on the tcgen05 kernels (N % 256 == 0) only
+  m->ln_folded = folded && m->d.dtype == TA_DTYPE_BF16 && (3 * m->d.dim) % 256 == 0 &&
+                 m->d.mlp_dim % 256 == 0;
   m->w.layers = m->layers.data();
   m->has_weights = true;
   return TA_OK;
@@ -315,6 +325,15 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
   const int D = d.dim, L = d.depth, N = m->n_tokens;
   const int act = d.dtype;
   const bool accumulate = d.prompt_mode == TA_PROMPT_ACCUMULATE;
+  // LayerNorm folded into the QKV / fc1 GEMMs (bf16 + folded weights registered): the
+  // producers of the residual emit xh = bf16(x) (in w.h) and row stats; no LN passes.
+  const bool fused = m->ln_folded && act == TA_DTYPE_BF16;
+  float* const ln1_stats = w.stats[0];
+  float* const ln2_stats = w.stats[1];
+  auto zero_stats = [&](float* buf, long long rows) {
+    cudaError_t e = cudaMemsetAsync(buf, 0, static_cast<size_t>(rows) * 8, st);
+    return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+  };
 
   // ---- patch embedding + cls + layer-0 prompts
   TA_TRY(patchify(images, w.patches, B, d.img, d.patch, m->kp, act, st));
@@ -326,11 +345,18 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
     e.rows_in = m->n_patches;
     e.rows_out = s.t[0];
     e.row_off = 1;
-    TA_TRY(linear(m, w.patches, m->w.patch_w, B * m->n_patches, D, m->kp, EPI_PATCH, e, st));
+    if (fused) {
+      TA_TRY(zero_stats(ln1_stats, static_cast<long long>(B) * s.t[0]));
+      e.xh = w.h;
+      e.stats = ln1_stats;
+    }
+    TA_TRY(linear(m, w.patches, m->w.patch_w, B * m->n_patches, D, m->kp,
+                  fused ? EPI_PATCH_STATS : EPI_PATCH, e, st));
   }
   TA_TRY(insert_rows(w.x[0], B, s.t[0], D, static_cast<const float*>(m->w.cls),
                      static_cast<const float*>(m->w.pos), ptab, task_ids, 0,
-                     gamma > 0 ? gamma : 0, N, st));
+                     gamma > 0 ? gamma : 0, N, st, fused ? w.h : nullptr,
+                     fused ? ln1_stats : nullptr));
 
   int cur = 0;
   const float* size = nullptr;
@@ -342,25 +368,41 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
     t = s.t[l];
     if (l > 0 && gamma > 0)
       TA_TRY(insert_rows(w.x[cur], B, t, D, nullptr, nullptr, ptab, task_ids, l, gamma,
-                         accumulate ? t - gamma : N, st));
+                         accumulate ? t - gamma : N, st, fused ? w.h : nullptr,
+                         fused ? ln1_stats : nullptr));
     const int M = B * t;
-    TA_TRY(layernorm(w.x[cur], static_cast<const float*>(Lw.ln1_w),
-                     static_cast<const float*>(Lw.ln1_b), w.h, M, D, act, st));
-    {
+    {  // LN1 + QKV
       GemmEpi e;
-      e.bias = static_cast<const float*>(Lw.qkv_b);
       e.out = w.qkv;
-      TA_TRY(linear(m, w.h, Lw.qkv_w, M, 3 * D, D, EPI_BIAS, e, st));
+      if (fused) {
+        e.ln_stats = ln1_stats;
+        e.c1 = static_cast<const float*>(Lw.qkv_c1);
+        e.c2 = static_cast<const float*>(Lw.qkv_c2);
+        e.inv_dim = 1.0f / D;
+        TA_TRY(linear(m, w.h, Lw.qkv_w_ln, M, 3 * D, D, EPI_LN_BIAS, e, st));
+      } else {
+        TA_TRY(layernorm(w.x[cur], static_cast<const float*>(Lw.ln1_w),
+                         static_cast<const float*>(Lw.ln1_b), w.h, M, D, act, st));
+        e.bias = static_cast<const float*>(Lw.qkv_b);
+        TA_TRY(linear(m, w.h, Lw.qkv_w, M, 3 * D, D, EPI_BIAS, e, st));
+      }
     }
     TA_TRY(attention(w.qkv, size, B, t, d.heads, m->hd, w.attn, act, st));
-    {
+    const int r = s.r[l];
+    {  // proj + residual (+ LN2 stats when no merge follows)
       GemmEpi e;
       e.bias = static_cast<const float*>(Lw.proj_b);
       e.resid = w.x[cur];
       e.out = w.x[cur];
-      TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID, e, st));
+      if (fused && r == 0) {
+        TA_TRY(zero_stats(ln2_stats, M));
+        e.xh = w.h;
+        e.stats = ln2_stats;
+        TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID_STATS, e, st));
+      } else {
+        TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID, e, st));
+      }
     }
-    const int r = s.r[l];
     int tp = t;
     if (r > 0) {
       const int na = (t + 1) / 2;
@@ -381,38 +423,53 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
                         cudaMemcpyDeviceToDevice, st);
       TA_TRY(merge(w.x[cur], size, B, t, D, r, src, dst, unm, static_cast<const float*>(Lw.ln2_w),
                    static_cast<const float*>(Lw.ln2_b), w.x[cur ^ 1], w.size[size_buf], w.h, act,
-                   st));
+                   st, fused ? ln2_stats : nullptr));
       cur ^= 1;
       size = w.size[size_buf];
       size_buf ^= 1;
       tp = t - r;
-    } else {
+    } else if (!fused) {
       TA_TRY(layernorm(w.x[cur], static_cast<const float*>(Lw.ln2_w),
                        static_cast<const float*>(Lw.ln2_b), w.h, M, D, act, st));
     }
     const int Mp = B * tp;
-    {
+    {  // LN2 + fc1 + GELU
       GemmEpi e;
-      e.bias = static_cast<const float*>(Lw.fc1_b);
       e.out = w.mlp;
-      TA_TRY(linear(m, w.h, Lw.fc1_w, Mp, d.mlp_dim, D, EPI_BIAS_GELU, e, st));
+      if (fused) {
+        e.ln_stats = ln2_stats;
+        e.c1 = static_cast<const float*>(Lw.fc1_c1);
+        e.c2 = static_cast<const float*>(Lw.fc1_c2);
+        e.inv_dim = 1.0f / D;
+        TA_TRY(linear(m, w.h, Lw.fc1_w_ln, Mp, d.mlp_dim, D, EPI_LN_GELU, e, st));
+      } else {
+        e.bias = static_cast<const float*>(Lw.fc1_b);
+        TA_TRY(linear(m, w.h, Lw.fc1_w, Mp, d.mlp_dim, D, EPI_BIAS_GELU, e, st));
+      }
     }
-    {
+    {  // fc2 + residual (+ next layer's LN1 stats)
       GemmEpi e;
       e.bias = static_cast<const float*>(Lw.fc2_b);
       e.resid = w.x[cur];
-      if (gamma > 0 && accumulate && l + 1 < L) {
+      const bool restride = gamma > 0 && accumulate && l + 1 < L;
+      const bool stats = fused && l + 1 < L;
+      if (restride) {
         // re-stride rows so the next layer's gamma prompt rows follow each image
         e.out = w.x[cur ^ 1];
         e.rows_in = tp;
         e.rows_out = s.t[l + 1];
         e.row_off = 0;
-        TA_TRY(linear(m, w.mlp, Lw.fc2_w, Mp, D, d.mlp_dim, EPI_BIAS_RESID, e, st));
-        cur ^= 1;
       } else {
         e.out = w.x[cur];
-        TA_TRY(linear(m, w.mlp, Lw.fc2_w, Mp, D, d.mlp_dim, EPI_BIAS_RESID, e, st));
       }
+      if (stats) {
+        TA_TRY(zero_stats(ln1_stats, static_cast<long long>(B) * s.t[l + 1]));
+        e.xh = w.h;
+        e.stats = ln1_stats;
+      }
+      TA_TRY(linear(m, w.mlp, Lw.fc2_w, Mp, D, d.mlp_dim,
+                    stats ? EPI_BIAS_RESID_STATS : EPI_BIAS_RESID, e, st));
+      if (restride) cur ^= 1;
     }
     t = tp;
   }

@@ -43,7 +43,7 @@ __device__ __forceinline__ void epi_load(const GemmEpi& e, int M, int N, long lo
   for (int q = 0; q < 8; ++q) {
     float4 v = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
                            __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
-    stage[lane * 8 + (q ^ (lane & 7))] = v;
+    sts_f4(smem_u32(stage) + 16u * (lane * 8 + (q ^ (lane & 7))), v);
   }
   __syncwarp();
   const int g = lane & 7;
@@ -52,11 +52,11 @@ __device__ __forceinline__ void epi_load(const GemmEpi& e, int M, int N, long lo
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int row = row0 + 4 * k;
-    c.v[k] = stage[row * 8 + (g ^ (row & 7))];
+    c.v[k] = lds_f4(smem_u32(stage) + 16u * (row * 8 + (g ^ (row & 7))));
   }
   __syncwarp();
   const bool full = m_base + 32 <= M;
-  if constexpr (EPI == EPI_BIAS_RESID) {
+  if constexpr (epi_is_resid(EPI)) {
     const float* rp = e.resid + (m_base + row0) * N + n;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -65,7 +65,7 @@ __device__ __forceinline__ void epi_load(const GemmEpi& e, int M, int N, long lo
       }
     }
   }
-  if constexpr (EPI == EPI_PATCH) {
+  if constexpr (epi_is_patch(EPI)) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const long long m = m_base + row0 + 4 * k;
@@ -75,15 +75,63 @@ __device__ __forceinline__ void epi_load(const GemmEpi& e, int M, int N, long lo
       }
     }
   }
+  if constexpr (epi_is_ln(EPI)) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const long long m = m_base + row0 + 4 * k;
+      if (full || m < M) {
+        const float2 st = __ldg(reinterpret_cast<const float2*>(e.ln_stats) + m);
+        c.x[k].x = st.x;
+        c.x[k].y = st.y;
+      }
+    }
+  }
+}
+
+// Per-row (sum, sumsq) partials of the values a warp stores, carried across the chunks of
+// one tile and flushed with one atomic pair per row (EPI_*_STATS).
+struct RowStats {
+  float s[8];
+  float q[8];
+};
+__device__ __forceinline__ void rowstats_clear(RowStats& r) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r.s[k] = r.q[k] = 0.f;
+}
+template <bool kRemap>
+__device__ __forceinline__ void rowstats_flush(const GemmEpi& e, int M, long long m_base, RowStats& r) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    float s = r.s[k], q = r.q[k];
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {  // the 8 lanes holding one row
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      q += __shfl_xor_sync(0xffffffffu, q, o);
+    }
+    const long long m = m_base + (lane >> 3) + 4 * k;
+    if ((lane & 7) == 0 && m < M) {
+      const long long orow = kRemap ? epi_out_row(e, m) : m;
+      atomicAdd(e.stats + 2 * orow, s);
+      atomicAdd(e.stats + 2 * orow + 1, q);
+    }
+  }
+  rowstats_clear(r);
 }
 
 template <int EPI, typename OutT, bool kRemap>
 __device__ __forceinline__ void epi_store(const GemmEpi& e, int M, int N, long long m_base, int n0,
-                                          const EpiChunk& c) {
+                                          const EpiChunk& c, RowStats& rs) {
   const uint32_t lane = lane_id();
   const int n = n0 + 4 * (lane & 7);
   const int row0 = lane >> 3;
-  const float4 b = __ldg(reinterpret_cast<const float4*>(e.bias + n));
+  float4 b, c1v;
+  if constexpr (epi_is_ln(EPI)) {
+    b = __ldg(reinterpret_cast<const float4*>(e.c2 + n));
+    c1v = __ldg(reinterpret_cast<const float4*>(e.c1 + n));
+  } else {
+    b = __ldg(reinterpret_cast<const float4*>(e.bias + n));
+  }
   const bool full = m_base + 32 <= M;
   OutT* obase = static_cast<OutT*>(e.out);
 #pragma unroll
@@ -91,17 +139,27 @@ __device__ __forceinline__ void epi_store(const GemmEpi& e, int M, int N, long l
     const long long m = m_base + row0 + 4 * k;
     if (!full && m >= M) continue;
     float4 w = c.v[k];
-    w.x += b.x;
-    w.y += b.y;
-    w.z += b.z;
-    w.w += b.w;
-    if constexpr (EPI == EPI_BIAS_RESID || EPI == EPI_PATCH) {
+    if constexpr (epi_is_ln(EPI)) {
+      const float mu = c.x[k].x * e.inv_dim;
+      const float var = fmaxf(c.x[k].y * e.inv_dim - mu * mu, 0.f);
+      const float rstd = rsqrtf(var + 1e-6f);
+      w.x = fmaf(rstd, fmaf(-mu, c1v.x, w.x), b.x);
+      w.y = fmaf(rstd, fmaf(-mu, c1v.y, w.y), b.y);
+      w.z = fmaf(rstd, fmaf(-mu, c1v.z, w.z), b.z);
+      w.w = fmaf(rstd, fmaf(-mu, c1v.w, w.w), b.w);
+    } else {
+      w.x += b.x;
+      w.y += b.y;
+      w.z += b.z;
+      w.w += b.w;
+    }
+    if constexpr (epi_is_resid(EPI) || epi_is_patch(EPI)) {
       w.x += c.x[k].x;
       w.y += c.x[k].y;
       w.z += c.x[k].z;
       w.w += c.x[k].w;
     }
-    if constexpr (EPI == EPI_BIAS_GELU) {
+    if constexpr (epi_is_gelu(EPI)) {
       w.x = gelu_erf_fast(w.x);
       w.y = gelu_erf_fast(w.y);
       w.z = gelu_erf_fast(w.z);
@@ -116,14 +174,35 @@ __device__ __forceinline__ void epi_store(const GemmEpi& e, int M, int N, long l
     } else {
       *reinterpret_cast<float4*>(obase + orow * N + n) = w;
     }
+    if constexpr (epi_is_stats(EPI)) {
+      uint2 pk;
+      pk.x = pack_bf16(w.x, w.y);
+      pk.y = pack_bf16(w.z, w.w);
+      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(e.xh) + orow * N + n) = pk;
+      rs.s[k] += (w.x + w.y) + (w.z + w.w);
+      rs.q[k] += (w.x * w.x + w.y * w.y) + (w.z * w.z + w.w * w.w);
+    }
   }
 }
 
 // ------------------------------------------------------------------ tcgen05 kernel
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 B rows -> SWIZZLE_128B
-constexpr int kEpiWarps = 8;
-constexpr int kGemmThreads = 128 + 32 * kEpiWarps;
+constexpr int kEpiWarps = 8;  // max epilogue warps (transpose staging is sized for this)
+// Epilogue warps per kind on the transposed-store path: the residual / patch / stats
+// epilogues keep two 32x32 chunks plus residual rows in flight and need the registers of a
+// 4-warp epilogue; the arithmetic-heavy ones (GELU, LN finish) use 8 warps.
+__host__ __device__ constexpr int epi_warps(int e) {
+  return (epi_is_resid(e) || epi_is_patch(e) || epi_is_stats(e)) ? 4 : 8;
+}
+__host__ __device__ constexpr int gemm_threads(int e) { return 128 + 32 * epi_warps(e); }
+// The CTA-pair kernel's TMA-store epilogue (no remap / stats / LN) is register-light: 8 warps.
+__host__ __device__ constexpr bool pair_tma(int e, bool remap) {
+  return !remap && !epi_is_stats(e) && !epi_is_ln(e);
+}
+__host__ __device__ constexpr int pair_epi_warps(int e, bool remap) {
+  return pair_tma(e, remap) ? 8 : epi_warps(e);
+}
 
 template <int BN>
 struct GemmCfg {
@@ -137,7 +216,7 @@ struct GemmCfg {
 };
 
 template <int BN, int EPI, typename OutT, bool kRemap>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(gemm_threads(EPI), 1)
     gemm_bf16_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
                            GemmEpi epi) {
@@ -167,7 +246,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 32 * kEpiWarps);
+      mbar_init(&tempty[a], epi_warps(EPI));  // one arrive per epilogue warp
     }
     fence_barrier_init();
   }
@@ -245,8 +324,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp >= 4) {
     const uint32_t ew = warp - 4;
     const uint32_t q = ew & 3;               // TMEM lane quarter (== warp % 4)
-    const int col0 = (ew >> 2) * (BN / 2);   // column half owned by this warp
-    constexpr int kChunks = BN / 2 / 32;
+    constexpr int kSplit = epi_warps(EPI) / 4;  // warps sharing one TMEM lane quarter
+    const int col0 = (ew >> 2) * (BN / kSplit);  // column range owned by this warp
+    constexpr int kChunks = BN / kSplit / 32;
     float4* stage = epi_stage + ew * 256;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -254,7 +334,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int m_blk = tile / num_n;
       const int n_blk = tile - m_blk * num_n;
       const long long m_base = static_cast<long long>(m_blk) * kBM + q * 32;
-      if constexpr (EPI == EPI_BIAS_RESID) {
+      if constexpr (epi_is_resid(EPI)) {
         // Pull this warp's residual rows (32 x BN/2 fp32) into L2 while the MMAs run.
         const long long m = m_base + lane;
         if (m < M)
@@ -265,7 +345,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * BN + col0;
       uint32_t r0[32], r1[32];
       EpiChunk ca, cb;
-      const bool live = m_base < M;
+      RowStats rs;
+      if constexpr (epi_is_stats(EPI)) rowstats_clear(rs);
+      const bool live = m_base < M && !epi.skip;
       const int nb = n_blk * BN + col0;
       static_assert(kChunks % 2 == 0, "chunk pairs");
       tmem_ld_32x32b_x32(t_row, r0);
@@ -277,18 +359,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tmem_ld_wait();
         if (c + 2 == kChunks) {
           tc_fence_before();
-          mbar_arrive(&tempty[acc]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
         }
         if (live) {
           epi_load<EPI>(epi, M, N, m_base, nb + (c + 1) * 32, r1, stage, cb);
-          epi_store<EPI, OutT, kRemap>(epi, M, N, m_base, nb + c * 32, ca);
+          epi_store<EPI, OutT, kRemap>(epi, M, N, m_base, nb + c * 32, ca, rs);
         }
         if (c + 2 < kChunks) {
           tmem_ld_32x32b_x32(t_row + (c + 2) * 32, r0);
           tmem_ld_wait();
           if (live) epi_load<EPI>(epi, M, N, m_base, nb + (c + 2) * 32, r0, stage, ca);
         }
-        if (live) epi_store<EPI, OutT, kRemap>(epi, M, N, m_base, nb + (c + 1) * 32, cb);
+        if (live) epi_store<EPI, OutT, kRemap>(epi, M, N, m_base, nb + (c + 1) * 32, cb, rs);
+      }
+      if constexpr (epi_is_stats(EPI)) {
+        if (live) rowstats_flush<kRemap>(epi, M, m_base, rs);
       }
       if (++acc == 2) {
         acc = 0;
@@ -311,28 +397,40 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // SM operand traffic per FLOP is 2/3 of the single-CTA 128 x 256 kernel and each SM's tensor
 // core reads half of B from the peer's smem.  The leader (rank 0) issues all MMAs; its
 // commits multicast to both CTAs' barriers; each CTA's epilogue drains its own 128 TMEM
-// lanes and releases the accumulator to the leader with a cluster-scope arrive.
-constexpr int kPairStages = 6;
+// lanes and releases the accumulator to the leader with a cluster-scope arrive (one per warp).
+//
+// Epilogue store path: kinds without a row remap / stats / LN finish write each 32-row x
+// 128-byte box of the output through a per-warp double-buffered smem staging box and a TMA
+// store (thread = row straight from tcgen05.ld: no transpose, no per-thread global stores,
+// rows >= M clipped by TMA); the others keep the transposed coalesced-store path.
+template <int EPI, typename OutT, bool kRemap>
 struct PairCfg {
+  static constexpr bool kTma = pair_tma(EPI, kRemap);
+  static constexpr int kWarps = pair_epi_warps(EPI, kRemap);
+  static constexpr int kThreads = 128 + 32 * kWarps;
   static constexpr int kABytes = 128 * kBK * 2;
   static constexpr int kBBytes = 128 * kBK * 2;  // this CTA's half of the 256-row W tile
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kEpiBytes = kEpiWarps * 32 * 32 * 4;
-  static constexpr int kSmemBytes = kPairStages * kStageBytes + kEpiBytes + 1024 + 256;
+  static constexpr int kEpiBytes = kTma ? kWarps * 2 * 4096 : kEpiWarps * 32 * 32 * 4;
+  static constexpr int kStages = kEpiBytes > 32768 ? 5 : 6;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 256;
 };
 
 template <int EPI, typename OutT, bool kRemap>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, kRemap>::kThreads, 1)
     gemm_bf16_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmA,
-                                const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                                const __grid_constant__ CUtensorMap tmB,
+                                const __grid_constant__ CUtensorMap tmC, int M, int N, int K,
                                 GemmEpi epi) {
+  using Cfg = PairCfg<EPI, OutT, kRemap>;
   constexpr int BN = 256;
-  constexpr int S = kPairStages;
+  constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  float4* epi_stage = reinterpret_cast<float4*>(smem + S * PairCfg::kStageBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * PairCfg::kStageBytes + PairCfg::kEpiBytes);
+  uint8_t* epi_smem = smem + S * Cfg::kStageBytes;
+  float4* epi_stage = reinterpret_cast<float4*>(epi_smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + Cfg::kEpiBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -346,6 +444,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if constexpr (Cfg::kTma) tma_prefetch(&tmC);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < S; ++s) {
@@ -354,7 +453,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 2 * 32 * kEpiWarps);  // both CTAs' epilogue threads (leader's copy)
+      mbar_init(&tempty[a], 2 * Cfg::kWarps);  // one arrive per epilogue warp of both CTAs
     }
     fence_barrier_init();
   }
@@ -383,9 +482,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         const int n_blk = tile - m_blk * num_n;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * PairCfg::kStageBytes;
-          uint8_t* sb = sa + PairCfg::kABytes;
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * PairCfg::kStageBytes);
+          uint8_t* sa = smem + stage * Cfg::kStageBytes;
+          uint8_t* sb = sa + Cfg::kABytes;
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::kStageBytes);
           const uint32_t fb = full_leader0 + stage * 8;
           tma_load_2d_pair(&tmA, fb, sa, kb * kBK, m_blk * 256 + rank * 128);
           tma_load_2d_pair(&tmB, fb, sb, kb * kBK, n_blk * BN + rank * 128);
@@ -410,8 +509,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * PairCfg::kStageBytes);
-          const uint32_t sb = sa + PairCfg::kABytes;
+          const uint32_t sa = smem_u32(smem + stage * Cfg::kStageBytes);
+          const uint32_t sb = sa + Cfg::kABytes;
           const uint64_t adesc = umma_desc_sw128(sa);
           const uint64_t bdesc = umma_desc_sw128(sb);
 #pragma unroll
@@ -433,55 +532,146 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   } else if (warp >= 4) {
     const uint32_t ew = warp - 4;
     const uint32_t q = ew & 3;
-    const int col0 = (ew >> 2) * (BN / 2);
-    constexpr int kChunks = BN / 2 / 32;
+    constexpr int kSplit = Cfg::kWarps / 4;          // warps sharing one TMEM lane quarter
+    const int col0 = (ew >> 2) * (BN / kSplit);      // column range owned by this warp
+    constexpr int kChunks = BN / kSplit / 32;
     float4* stage = epi_stage + ew * 256;
     const uint32_t tempty_leader0 = mapa_shared(&tempty[0], 0);
     int acc = 0;
     uint32_t acc_phase = 0;
+    int tma_buf = 0;
     for (int tile = cid; tile < num_tiles; tile += ncl) {
       const int m_blk = tile / num_n;
       const int n_blk = tile - m_blk * num_n;
       const long long m_base = static_cast<long long>(m_blk) * 256 + rank * 128 + q * 32;
-      if constexpr (EPI == EPI_BIAS_RESID) {
+      if constexpr (epi_is_resid(EPI)) {
+        // Pull this warp's residual rows into L2 while the MMAs run.
         const long long m = m_base + lane;
         if (m < M)
-          prefetch_l2_bulk(epi.resid + m * N + n_blk * BN + col0, BN / 2 * sizeof(float));
+          prefetch_l2_bulk(epi.resid + m * N + n_blk * BN + col0, BN / kSplit * sizeof(float));
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * BN + col0;
-      uint32_t r0[32], r1[32];
-      EpiChunk ca, cb;
-      const bool live = m_base < M;
-      const int nb = n_blk * BN + col0;
-      tmem_ld_32x32b_x32(t_row, r0);
-      tmem_ld_wait();
-      if (live) epi_load<EPI>(epi, M, N, m_base, nb, r0, stage, ca);
+      if constexpr (Cfg::kTma) {
+        // ---- thread = row; bias / GELU / residual in registers; TMA store per 128-byte box
+        constexpr int CW = 128 / static_cast<int>(sizeof(OutT));  // columns per box
+        constexpr int NCH = (BN / kSplit) / CW;
+        const long long m = m_base + lane;
+        const bool row_ok = m < M;
 #pragma unroll 1
-      for (int c = 0; c < kChunks; c += 2) {
-        tmem_ld_32x32b_x32(t_row + (c + 1) * 32, r1);
+        for (int c = 0; c < NCH; ++c) {
+          const int n0 = n_blk * BN + col0 + c * CW;
+          float v[CW];
+          {
+            uint32_t r[CW];
+#pragma unroll
+            for (int g = 0; g < CW / 32; ++g)
+              tmem_ld_32x32b_x32(t_row + c * CW + 32 * g, *reinterpret_cast<uint32_t(*)[32]>(&r[32 * g]));
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < CW; ++j) v[j] = __uint_as_float(r[j]);
+          }
+          if (c + 1 == NCH) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
+          }
+          if (epi.skip) continue;
+          if constexpr (epi_is_resid(EPI)) {
+            if (row_ok) {
+              const float4* rp = reinterpret_cast<const float4*>(epi.resid + m * N + n0);
+              float4 rr[CW / 4];
+#pragma unroll
+              for (int j = 0; j < CW / 4; ++j) rr[j] = rp[j];
+#pragma unroll
+              for (int j = 0; j < CW / 4; ++j) {
+                v[4 * j] += rr[j].x;
+                v[4 * j + 1] += rr[j].y;
+                v[4 * j + 2] += rr[j].z;
+                v[4 * j + 3] += rr[j].w;
+              }
+            }
+          }
+          const float4* bp = reinterpret_cast<const float4*>(epi.bias + n0);
+#pragma unroll
+          for (int j = 0; j < CW / 4; ++j) {
+            const float4 b = __ldg(bp + j);
+            v[4 * j] += b.x;
+            v[4 * j + 1] += b.y;
+            v[4 * j + 2] += b.z;
+            v[4 * j + 3] += b.w;
+          }
+          if constexpr (epi_is_gelu(EPI)) {
+#pragma unroll
+            for (int j = 0; j < CW; ++j) v[j] = gelu_erf_fast(v[j]);
+          }
+          uint8_t* sbuf = epi_smem + (ew * 2 + tma_buf) * 4096;
+          if (lane == 0) bulk_wait_group_read<1>();  // the store that last used sbuf has read it
+          __syncwarp();
+          const uint32_t srow = smem_u32(sbuf) + lane * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {  // 16-byte chunk j of this row, SW128 position j ^ (row & 7)
+            uint4 w;
+            if constexpr (sizeof(OutT) == 2) {
+              w = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                             pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+            } else {
+              w = make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                             __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+            }
+            sts_u4(srow + ((j ^ (lane & 7)) << 4), w);
+          }
+          fence_proxy_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, sbuf, n0, static_cast<int32_t>(m_base));
+            bulk_commit_group();
+          }
+          tma_buf ^= 1;
+        }
+      } else {
+        uint32_t r0[32], r1[32];
+        EpiChunk ca, cb;
+        RowStats rs;
+        if constexpr (epi_is_stats(EPI)) rowstats_clear(rs);
+        const bool live = m_base < M && !epi.skip;
+        const int nb = n_blk * BN + col0;
+        tmem_ld_32x32b_x32(t_row, r0);
         tmem_ld_wait();
-        if (c + 2 == kChunks) {
-          tc_fence_before();
-          mbar_arrive_remote(tempty_leader0 + acc * 8);
-        }
-        if (live) {
-          epi_load<EPI>(epi, M, N, m_base, nb + (c + 1) * 32, r1, stage, cb);
-          epi_store<EPI, OutT, kRemap>(epi, M, N, m_base, nb + c * 32, ca);
-        }
-        if (c + 2 < kChunks) {
-          tmem_ld_32x32b_x32(t_row + (c + 2) * 32, r0);
+        if (live) epi_load<EPI>(epi, M, N, m_base, nb, r0, stage, ca);
+#pragma unroll 1
+        for (int c = 0; c < kChunks; c += 2) {
+          tmem_ld_32x32b_x32(t_row + (c + 1) * 32, r1);
           tmem_ld_wait();
-          if (live) epi_load<EPI>(epi, M, N, m_base, nb + (c + 2) * 32, r0, stage, ca);
+          if (c + 2 == kChunks) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
+          }
+          if (live) {
+            epi_load<EPI>(epi, M, N, m_base, nb + (c + 1) * 32, r1, stage, cb);
+            epi_store<EPI, OutT, kRemap>(epi, M, N, m_base, nb + c * 32, ca, rs);
+          }
+          if (c + 2 < kChunks) {
+            tmem_ld_32x32b_x32(t_row + (c + 2) * 32, r0);
+            tmem_ld_wait();
+            if (live) epi_load<EPI>(epi, M, N, m_base, nb + (c + 2) * 32, r0, stage, ca);
+          }
+          if (live) epi_store<EPI, OutT, kRemap>(epi, M, N, m_base, nb + (c + 1) * 32, cb, rs);
         }
-        if (live) epi_store<EPI, OutT, kRemap>(epi, M, N, m_base, nb + (c + 1) * 32, cb);
+        if constexpr (epi_is_stats(EPI)) {
+          if (live) rowstats_flush<kRemap>(epi, M, m_base, rs);
+        }
       }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+  }
+  if constexpr (Cfg::kTma) {
+    if (warp >= 4 && lane == 0) bulk_wait_group<0>();  // staged boxes fully stored
   }
   grid_dep_launch();
   tc_fence_before();
@@ -609,7 +799,7 @@ static int launch_bf16(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
   const int grid = tiles < device_sm_count() ? tiles : device_sm_count();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kGemmThreads);
+  cfg.blockDim = dim3(gemm_threads(EPI));
   cfg.dynamicSmemBytes = Cfg::kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -621,30 +811,53 @@ static int launch_bf16(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 
+// Output tensor map for the TMA-store epilogue: [M, N] row-major, 32-row x 128-byte boxes, SW128.
+static int make_tmap_out(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                         bool bf16) {
+  auto enc = get_encode_fn();
+  if (!enc) return TA_ERR_CUDA;
+  const uint64_t es = bf16 ? 2 : 4;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * es};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / es), 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? TA_OK : TA_ERR_SHAPE;
+}
+
 template <int EPI, typename OutT, bool kRemap = false>
 static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, int N, int K,
                        const GemmEpi& epi, cudaStream_t stream) {
+  using Cfg = PairCfg<EPI, OutT, kRemap>;
   auto kern = gemm_bf16_sm100_pair_kernel<EPI, OutT, kRemap>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         PairCfg::kSmemBytes);
+                                         Cfg::kSmemBytes);
     if (e != cudaSuccess) return set_last_cuda_error(e);
     attr_set = true;
+  }
+  CUtensorMap tc_{};
+  if (Cfg::kTma) {
+    const int rc = make_tmap_out(&tc_, epi.out, M, N, sizeof(OutT) == 2);
+    if (rc) return rc;
   }
   const int tiles = ((M + 255) / 256) * (N / 256);
   const int pairs = device_sm_count() / 2;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * (tiles < pairs ? tiles : pairs));
-  cfg.blockDim = dim3(kGemmThreads);
-  cfg.dynamicSmemBytes = PairCfg::kSmemBytes;
+  cfg.blockDim = dim3(Cfg::kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta_, tb_, M, N, K, epi);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta_, tb_, tc_, M, N, K, epi);
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 
@@ -662,6 +875,15 @@ static int dispatch_pair(const CUtensorMap& a, const CUtensorMap& b, int M, int 
                          : launch_pair<EPI_BIAS_RESID, float, false>(a, b, M, N, K, epi, s);
     case EPI_PATCH:
       return launch_pair<EPI_PATCH, float, true>(a, b, M, N, K, epi, s);
+    case EPI_BIAS_RESID_STATS:
+      return epi.rows_in ? launch_pair<EPI_BIAS_RESID_STATS, float, true>(a, b, M, N, K, epi, s)
+                         : launch_pair<EPI_BIAS_RESID_STATS, float, false>(a, b, M, N, K, epi, s);
+    case EPI_PATCH_STATS:
+      return launch_pair<EPI_PATCH_STATS, float, true>(a, b, M, N, K, epi, s);
+    case EPI_LN_BIAS:
+      return launch_pair<EPI_LN_BIAS, __nv_bfloat16>(a, b, M, N, K, epi, s);
+    case EPI_LN_GELU:
+      return launch_pair<EPI_LN_GELU, __nv_bfloat16>(a, b, M, N, K, epi, s);
   }
   return TA_ERR_INVALID;
 }
@@ -691,15 +913,31 @@ static int dispatch_bf16(const CUtensorMap& a, const CUtensorMap& b, int M, int 
                          : launch_bf16<BN, EPI_BIAS_RESID, float, false>(a, b, M, N, K, epi, s);
     case EPI_PATCH:
       return launch_bf16<BN, EPI_PATCH, float, true>(a, b, M, N, K, epi, s);
+    case EPI_BIAS_RESID_STATS:
+      return epi.rows_in ? launch_bf16<BN, EPI_BIAS_RESID_STATS, float, true>(a, b, M, N, K, epi, s)
+                         : launch_bf16<BN, EPI_BIAS_RESID_STATS, float, false>(a, b, M, N, K, epi, s);
+    case EPI_PATCH_STATS:
+      return launch_bf16<BN, EPI_PATCH_STATS, float, true>(a, b, M, N, K, epi, s);
+    case EPI_LN_BIAS:
+      return launch_bf16<BN, EPI_LN_BIAS, __nv_bfloat16>(a, b, M, N, K, epi, s);
+    case EPI_LN_GELU:
+      return launch_bf16<BN, EPI_LN_GELU, __nv_bfloat16>(a, b, M, N, K, epi, s);
   }
   return TA_ERR_INVALID;
 }
 
 int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, bool out_bf16,
-              const GemmEpi& epi, cudaStream_t stream) {
+              const GemmEpi& epi_in, cudaStream_t stream) {
+  static const int skip_epi = [] {
+    const char* v = getenv("TA_GEMM_SKIP_EPILOGUE");  // profiling only: mainloop without epilogue
+    return v && v[0] == '1';
+  }();
+  GemmEpi epi = epi_in;
+  epi.skip = skip_epi;
   if (M <= 0) return TA_OK;
   if (K % kBK != 0 || N % 128 != 0) return TA_ERR_SHAPE;
-  if ((epi_kind == EPI_BIAS_RESID || epi_kind == EPI_PATCH) && out_bf16) return TA_ERR_INVALID;
+  if ((epi_is_resid(epi_kind) || epi_is_patch(epi_kind)) && out_bf16) return TA_ERR_INVALID;
+  if (epi_is_ln(epi_kind) && !out_bf16) return TA_ERR_INVALID;
   const int BN = (N % 256 == 0) ? 256 : 128;
   CUtensorMap ta_, tb_;
   int rc = make_tmap_bf16_2d(&ta_, A, M, K, kBM);

@@ -74,25 +74,54 @@ __global__ void insert_rows_kernel(float* __restrict__ x, int t_total, int D,
                                    const float* __restrict__ cls, const float* __restrict__ pos,
                                    const float* const* __restrict__ prompt_tab,
                                    const int32_t* __restrict__ task_ids, int layer, int gamma,
-                                   int prompt_row) {
+                                   int prompt_row, __nv_bfloat16* __restrict__ xh,
+                                   float* __restrict__ stats) {
+  // One warp per inserted row; with xh / stats (LayerNorm folded into the QKV GEMM) the
+  // row is also written as bf16 and its exact (sum, sumsq) stored.
   const int b = blockIdx.x;
-  float* xb = x + static_cast<long long>(b) * t_total * D;
-  if (cls != nullptr) {
-    for (int c = threadIdx.x; c < D; c += blockDim.x) xb[c] = cls[c] + pos[c];
-  }
-  if (gamma > 0) {
-    const float* P = prompt_tab[task_ids[b]] + static_cast<long long>(layer) * gamma * D;
-    float4* dst = reinterpret_cast<float4*>(xb + static_cast<long long>(prompt_row) * D);
-    const float4* src = reinterpret_cast<const float4*>(P);
-    for (int i = threadIdx.x; i < gamma * D / 4; i += blockDim.x) dst[i] = src[i];
+  const int n_cls = cls != nullptr ? 1 : 0;
+  const int n_rows = n_cls + (gamma > 0 ? gamma : 0);
+  const float* P = gamma > 0 ? prompt_tab[task_ids[b]] + static_cast<long long>(layer) * gamma * D
+                             : nullptr;
+  const int lane = lane_id();
+  for (int rr = warp_id(); rr < n_rows; rr += blockDim.x / 32) {
+    const bool is_cls = rr < n_cls;
+    const long long row = static_cast<long long>(b) * t_total + (is_cls ? 0 : prompt_row + rr - n_cls);
+    const float* srow = is_cls ? nullptr : P + static_cast<long long>(rr - n_cls) * D;
+    float s = 0.f, q = 0.f;
+    for (int c = 4 * lane; c < D; c += 128) {
+      float4 v;
+      if (is_cls) {
+        const float4 a = *reinterpret_cast<const float4*>(cls + c);
+        const float4 p = *reinterpret_cast<const float4*>(pos + c);
+        v = make_float4(a.x + p.x, a.y + p.y, a.z + p.z, a.w + p.w);
+      } else {
+        v = *reinterpret_cast<const float4*>(srow + c);
+      }
+      *reinterpret_cast<float4*>(x + row * D + c) = v;
+      if (xh != nullptr) {
+        uint2 pk;
+        pk.x = pack_bf16(v.x, v.y);
+        pk.y = pack_bf16(v.z, v.w);
+        *reinterpret_cast<uint2*>(xh + row * D + c) = pk;
+        s += (v.x + v.y) + (v.z + v.w);
+        q += (v.x * v.x + v.y * v.y) + (v.z * v.z + v.w * v.w);
+      }
+    }
+    if (stats != nullptr) {
+      s = warp_sum(s);
+      q = warp_sum(q);
+      if (lane == 0) *reinterpret_cast<float2*>(stats + 2 * row) = make_float2(s, q);
+    }
   }
 }
 
 int insert_rows(float* x, int B, int t_total, int D, const float* cls, const float* pos,
                 const float* const* prompt_tab, const int32_t* task_ids, int layer, int gamma,
-                int prompt_row, cudaStream_t s) {
+                int prompt_row, cudaStream_t s, void* xh, float* stats) {
+  if (D % 128 != 0) return TA_ERR_SHAPE;
   insert_rows_kernel<<<B, 256, 0, s>>>(x, t_total, D, cls, pos, prompt_tab, task_ids, layer,
-                                       gamma, prompt_row);
+                                       gamma, prompt_row, static_cast<__nv_bfloat16*>(xh), stats);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }

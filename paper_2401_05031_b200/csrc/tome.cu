@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(256)
                  const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                  const int32_t* __restrict__ unm, const float* __restrict__ ln_w,
                  const float* __restrict__ ln_b, float* __restrict__ x_out,
-                 float* __restrict__ size_out, T* __restrict__ h_out) {
+                 float* __restrict__ size_out, T* __restrict__ h_out, float* __restrict__ stats_out) {
   constexpr int D = 128 * VEC;
   __shared__ int s_src[256];
   __shared__ int s_dst[256];
@@ -252,6 +252,22 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int i = 0; i < VEC; ++i) xo[lane + 32 * i] = acc[i];
     if (lane == 0) size_out[orow] = stot;
+    if (stats_out != nullptr) {
+      // LayerNorm folded into fc1 (bf16 path): xh = bf16(x') and exact row (sum, sumsq)
+      float q2 = 0.f;
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        const int cidx = 4 * (lane + 32 * i);
+        q2 += (acc[i].x * acc[i].x + acc[i].y * acc[i].y) + (acc[i].z * acc[i].z + acc[i].w * acc[i].w);
+        uint2 p;
+        p.x = pack_bf16(acc[i].x, acc[i].y);
+        p.y = pack_bf16(acc[i].z, acc[i].w);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(h_out) + orow * D + cidx) = p;
+      }
+      const float s_all = warp_sum(sum), q_all = warp_sum(q2);
+      if (lane == 0) *reinterpret_cast<float2*>(stats_out + 2 * orow) = make_float2(s_all, q_all);
+      continue;
+    }
     // fused LN2
     const float mean = warp_sum(sum) / D;
     float q = 0.f;
@@ -288,7 +304,7 @@ template <typename T>
 static int merge_dispatch(const float* x, const float* size, int B, int t, int D, int r,
                           const int32_t* src, const int32_t* dst, const int32_t* unm,
                           const float* ln_w, const float* ln_b, float* x_out, float* size_out,
-                          T* h_out, cudaStream_t s) {
+                          T* h_out, float* stats_out, cudaStream_t s) {
   const int tp = t - r;
   const int rows_per_cta = 8 * 4;
   cudaLaunchConfig_t cfg = {};
@@ -304,7 +320,7 @@ static int merge_dispatch(const float* x, const float* size, int B, int t, int D
 #define TA_MERGE_CASE(DIM, V)                                                                  \
   case DIM:                                                                                    \
     e = cudaLaunchKernelEx(&cfg, merge_kernel<V, T>, x, size, t, r, src, dst, unm, ln_w, ln_b, \
-                           x_out, size_out, h_out);                                            \
+                           x_out, size_out, h_out, stats_out);                                 \
     break;
   switch (D) {
     TA_MERGE_CASE(256, 2)
@@ -319,13 +335,15 @@ static int merge_dispatch(const float* x, const float* size, int B, int t, int D
 
 int merge(const float* x, const float* size, int B, int t, int D, int r, const int32_t* src,
           const int32_t* dst, const int32_t* unm, const float* ln_w, const float* ln_b,
-          float* x_out, float* size_out, void* h_out, int h_dtype, cudaStream_t s) {
+          float* x_out, float* size_out, void* h_out, int h_dtype, cudaStream_t s,
+          float* stats_out) {
+  if (stats_out != nullptr && h_dtype != TA_DTYPE_BF16) return TA_ERR_INVALID;
   if (r <= 0 || r > (t + 1) / 2 - 1 || r > 256) return TA_ERR_INVALID;
   if (h_dtype == TA_DTYPE_BF16)
     return merge_dispatch(x, size, B, t, D, r, src, dst, unm, ln_w, ln_b, x_out, size_out,
-                          static_cast<__nv_bfloat16*>(h_out), s);
+                          static_cast<__nv_bfloat16*>(h_out), stats_out, s);
   return merge_dispatch(x, size, B, t, D, r, src, dst, unm, ln_w, ln_b, x_out, size_out,
-                        static_cast<float*>(h_out), s);
+                        static_cast<float*>(h_out), stats_out, s);
 }
 
 }  // namespace ta

@@ -50,12 +50,15 @@ class TransformerModel:
 
     def __init__(self, cfg: ViTConfig, params: Dict[str, object], device: Union[str, torch.device] = "cuda:0",
                  dtype: str = "bf16", prompt_mode: str = "accumulate", n_tasks: int = 1,
-                 max_classes: int = 100):
+                 max_classes: int = 100, fold_ln: Optional[bool] = None):
         if dtype not in _DTYPES:
             raise ConfigError(f"dtype must be one of {sorted(_DTYPES)}")
         if prompt_mode not in PROMPT_MODES:
             raise ConfigError(f"prompt_mode must be one of {PROMPT_MODES}")
         self.cfg, self.dtype, self.prompt_mode = cfg, dtype, prompt_mode
+        # bf16 mode folds LayerNorm into the QKV / fc1 GEMMs by default (fp32 parity mode
+        # keeps the explicit LayerNorm passes)
+        self.fold_ln = False if fold_ln is None else bool(fold_ln and dtype == "bf16")
         self.device = torch.device(device)
         if self.device.type != "cuda":
             raise ConfigError("TransformerModel runs on a CUDA device only (no CPU fallback)")
@@ -96,6 +99,16 @@ class TransformerModel:
                 vals[k] = _ptr(self._mat(lw[k]))
             for k in ("ln1_w", "ln1_b", "qkv_b", "proj_b", "ln2_w", "ln2_b", "fc1_b", "fc2_b"):
                 vals[k] = _ptr(self._vec(lw[k]))
+            if self.fold_ln:
+                # LayerNorm folded into the following GEMM (include/tokadapt_cuda.h):
+                # W' = bf16(W o gamma), c1 = rowsum(W') (of the rounded values), c2 = W beta + b
+                for name, ln in (("qkv", "ln1"), ("fc1", "ln2")):
+                    w32 = lw[f"{name}_w"].double()
+                    wf = (w32 * lw[f"{ln}_w"].double()[None, :]).to(torch.bfloat16)
+                    vals[f"{name}_w_ln"] = _ptr(self._mat(wf))
+                    vals[f"{name}_c1"] = _ptr(self._vec(wf.double().sum(dim=1).float()))
+                    c2 = w32 @ lw[f"{ln}_b"].double() + lw[f"{name}_b"].double()
+                    vals[f"{name}_c2"] = _ptr(self._vec(c2.float()))
             layers[i] = _cuda.LayerWeights(**vals)
         self._layers_c = layers
         self._weights_c = _cuda.Weights(

@@ -40,12 +40,13 @@ def oracle_forward(cfg, params, tasks, images, task_ids, gamma, prompt_mode="acc
                               dtype=dtype, forced=forced, max_classes=max_classes)
 
 
-def serve_model(cfg, params, tasks, dtype="bf16", prompt_mode="accumulate", max_classes=None):
+def serve_model(cfg, params, tasks, dtype="bf16", prompt_mode="accumulate", max_classes=None,
+                fold_ln=None):
     from paper_2401_05031_b200.model import ServeModel, TaskModel, TransformerModel
 
     mc = max_classes or max(t["head"]["w"].shape[0] for t in tasks)
     bb = TransformerModel(cfg, params, "cuda:0", dtype=dtype, prompt_mode=prompt_mode,
-                          n_tasks=len(tasks), max_classes=mc)
+                          n_tasks=len(tasks), max_classes=mc, fold_ln=fold_ln)
     sm = ServeModel(bb)
     for t in tasks:
         sm.register_task(TaskModel(t["name"], t["head"]["w"], t["head"]["b"], dict(t["prompts"])))

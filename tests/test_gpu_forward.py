@@ -17,13 +17,14 @@ pytestmark = pytest.mark.gpu
 BF16_TOL = 0.03  # relative to max|logit| of the oracle, index-forced
 
 
-def _run(name, gamma, batch, dtype, prompt_mode="accumulate", classes=(10, 100), seed=0):
+def _run(name, gamma, batch, dtype, prompt_mode="accumulate", classes=(10, 100), seed=0,
+         fold_ln=None):
     cfg, params = helpers.backbone(name)
     tasks = helpers.task_params(cfg, classes, [gamma] if gamma > 0 else [])
     imgs = helpers.synthetic_images(batch, cfg.img, seed=seed)
     task_ids = torch.arange(batch, dtype=torch.int64) % len(classes)
     ref, tr = helpers.oracle_forward(cfg, params, tasks, imgs, task_ids, gamma, prompt_mode)
-    sm = helpers.serve_model(cfg, params, tasks, dtype=dtype, prompt_mode=prompt_mode)
+    sm = helpers.serve_model(cfg, params, tasks, dtype=dtype, prompt_mode=prompt_mode, fold_ln=fold_ln)
     bb = sm.backbone
     n_tr = bb.trace_len(batch, gamma)
     trace = torch.full((max(n_tr, 1),), -1, dtype=torch.int32, device="cuda")
@@ -63,12 +64,13 @@ def test_tiny_fp32(gamma, prompt_mode):
     torch.testing.assert_close(_finite(out), _finite(ref), rtol=1e-4, atol=1e-4 * scale)
 
 
-@pytest.mark.parametrize("gamma", [-8, 0, 8])
+@pytest.mark.parametrize("gamma", [-8, -1, 0, 8])
 @pytest.mark.parametrize("prompt_mode", ["accumulate", "replace"])
-def test_tiny_bf16(gamma, prompt_mode):
+@pytest.mark.parametrize("fold_ln", [True, False])
+def test_tiny_bf16(gamma, prompt_mode, fold_ln):
     if gamma <= 0 and prompt_mode == "replace":
         pytest.skip("prompt mode only matters for gamma > 0")
-    cfg, ref, tr, out, gtr, forced, _ = _run("vit_tiny", gamma, 6, "bf16", prompt_mode)
+    cfg, ref, tr, out, gtr, forced, _ = _run("vit_tiny", gamma, 6, "bf16", prompt_mode, fold_ln=fold_ln)
     scale = _finite(ref).abs().max().item()
     err = (_finite(forced) - _finite(ref)).abs().max().item()
     assert err <= BF16_TOL * scale, (err, scale)
@@ -82,8 +84,9 @@ def test_vit_b16_config1_fp32():
     torch.testing.assert_close(_finite(out), _finite(ref), rtol=1e-4, atol=1e-4 * scale)
 
 
-def test_vit_b16_config1_bf16():
-    cfg, ref, tr, out, gtr, forced, _ = _run("vit_b16", -8, 8, "bf16")
+@pytest.mark.parametrize("fold_ln", [True, False])
+def test_vit_b16_config1_bf16(fold_ln):
+    cfg, ref, tr, out, gtr, forced, _ = _run("vit_b16", -8, 8, "bf16", fold_ln=fold_ln)
     fr, rf = _finite(forced), _finite(ref)
     scale = rf.abs().max().item()
     bound = BF16_TOL * scale
@@ -93,3 +96,13 @@ def test_vit_b16_config1_bf16():
     margin = top2[:, 0] - top2[:, 1]
     decisive = margin > 2 * bound
     assert torch.equal(fr.argmax(-1)[decisive], rf.argmax(-1)[decisive])
+    print(f"bf16 fold_ln={fold_ln}: max|dlogit| {err:.3e} (bound {bound:.3e}, max|logit| {scale:.3f})")
+
+
+@pytest.mark.parametrize("gamma", [-16, 0, 16])
+def test_vit_b16_bf16_sweep_gammas(gamma):
+    """The bench's gammas at batch 16 (bf16, LN folded), index-forced."""
+    cfg, ref, tr, out, gtr, forced, _ = _run("vit_b16", gamma, 16, "bf16")
+    fr, rf = _finite(forced), _finite(ref)
+    scale = rf.abs().max().item()
+    assert (fr - rf).abs().max().item() <= BF16_TOL * scale
