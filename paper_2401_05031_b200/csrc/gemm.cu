@@ -198,7 +198,7 @@ __host__ __device__ constexpr int epi_warps(int e) {
 __host__ __device__ constexpr int gemm_threads(int e) { return 128 + 32 * epi_warps(e); }
 // The CTA-pair kernel's TMA-store epilogue (no remap / stats / LN) is register-light: 8 warps.
 __host__ __device__ constexpr bool pair_tma(int e, bool remap) {
-  return !remap && !epi_is_stats(e) && !epi_is_ln(e);
+  return !epi_is_stats(e) && !epi_is_ln(e);
 }
 __host__ __device__ constexpr int pair_epi_warps(int e, bool remap) {
   return pair_tma(e, remap) ? 8 : epi_warps(e);
@@ -578,9 +578,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
             if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
           }
           if (epi.skip) continue;
-          if constexpr (epi_is_resid(EPI)) {
+          if constexpr (epi_is_resid(EPI) || epi_is_patch(EPI)) {
             if (row_ok) {
-              const float4* rp = reinterpret_cast<const float4*>(epi.resid + m * N + n0);
+              const float4* rp =
+                  epi_is_resid(EPI)
+                      ? reinterpret_cast<const float4*>(epi.resid + m * N + n0)
+                      : reinterpret_cast<const float4*>(epi.pos + (epi.row_off + m % epi.rows_in) * N + n0);
               float4 rr[CW / 4];
 #pragma unroll
               for (int j = 0; j < CW / 4; ++j) rr[j] = rp[j];
@@ -610,6 +613,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           if (lane == 0) bulk_wait_group_read<1>();  // the store that last used sbuf has read it
           __syncwarp();
           const uint32_t srow = smem_u32(sbuf) + lane * 128;
+          // Row remap: a row of this box that belongs to the next image is also stored
+          // directly (the box's TMA store lands it in this image's prompt / padding slots,
+          // which insert_rows rewrites, or clips it past rows_out).
+          uint4* spill_row = nullptr;
+          if constexpr (kRemap) {
+            const int b = static_cast<int>(m_base / epi.rows_in);
+            const int i = static_cast<int>(m_base - static_cast<long long>(b) * epi.rows_in) + lane;
+            if (i >= epi.rows_in && row_ok) {  // image b + i / rows_in (short images: >1 boundary)
+              const int bi = i / epi.rows_in;
+              spill_row = reinterpret_cast<uint4*>(
+                  static_cast<OutT*>(epi.out) +
+                  (static_cast<long long>(b + bi) * epi.rows_out + epi.row_off + i - bi * epi.rows_in) * N +
+                  n0);
+            }
+          }
 #pragma unroll
           for (int j = 0; j < 8; ++j) {  // 16-byte chunk j of this row, SW128 position j ^ (row & 7)
             uint4 w;
@@ -621,11 +639,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
                              __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
             }
             sts_u4(srow + ((j ^ (lane & 7)) << 4), w);
+            if (kRemap && spill_row != nullptr) spill_row[j] = w;
           }
           fence_proxy_async_shared();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmC, sbuf, n0, static_cast<int32_t>(m_base));
+            if constexpr (kRemap) {
+              // 3D view [B][rows_out][N]: the box goes to image b at its in-image row.
+              const int b = static_cast<int>(m_base / epi.rows_in);
+              const int i0 = static_cast<int>(m_base - static_cast<long long>(b) * epi.rows_in);
+              tma_store_3d(&tmC, sbuf, n0, epi.row_off + i0, b);
+            } else {
+              tma_store_2d(&tmC, sbuf, n0, static_cast<int32_t>(m_base));
+            }
             bulk_commit_group();
           }
           tma_buf ^= 1;
@@ -828,6 +854,23 @@ static int make_tmap_out(CUtensorMap* map, const void* base, uint64_t rows, uint
   return r == CUDA_SUCCESS ? TA_OK : TA_ERR_SHAPE;
 }
 
+// 3D view [B][rows_out][N] of a row-remapped output, same 32-row x 128-byte boxes.
+static int make_tmap_out3(CUtensorMap* map, const void* base, uint64_t images, uint64_t rows_out,
+                          uint64_t cols, bool bf16) {
+  auto enc = get_encode_fn();
+  if (!enc) return TA_ERR_CUDA;
+  const uint64_t es = bf16 ? 2 : 4;
+  cuuint64_t dims[3] = {cols, rows_out, images};
+  cuuint64_t strides[2] = {cols * es, rows_out * cols * es};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(128 / es), 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? TA_OK : TA_ERR_SHAPE;
+}
+
 template <int EPI, typename OutT, bool kRemap = false>
 static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, int N, int K,
                        const GemmEpi& epi, cudaStream_t stream) {
@@ -842,7 +885,8 @@ static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
   }
   CUtensorMap tc_{};
   if (Cfg::kTma) {
-    const int rc = make_tmap_out(&tc_, epi.out, M, N, sizeof(OutT) == 2);
+    const int rc = kRemap ? make_tmap_out3(&tc_, epi.out, M / epi.rows_in, epi.rows_out, N, sizeof(OutT) == 2)
+                          : make_tmap_out(&tc_, epi.out, M, N, sizeof(OutT) == 2);
     if (rc) return rc;
   }
   const int tiles = ((M + 255) / 256) * (N / 256);
