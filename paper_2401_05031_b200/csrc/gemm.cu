@@ -197,9 +197,7 @@ __host__ __device__ constexpr int epi_warps(int e) {
 }
 __host__ __device__ constexpr int gemm_threads(int e) { return 128 + 32 * epi_warps(e); }
 // The CTA-pair kernel's TMA-store epilogue (no remap / stats / LN) is register-light: 8 warps.
-__host__ __device__ constexpr bool pair_tma(int e, bool remap) {
-  return !epi_is_stats(e) && !epi_is_ln(e);
-}
+__host__ __device__ constexpr bool pair_tma(int e, bool remap) { return true; }
 __host__ __device__ constexpr int pair_epi_warps(int e, bool remap) {
   return pair_tma(e, remap) ? 8 : epi_warps(e);
 }
@@ -406,12 +404,14 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
 template <int EPI, typename OutT, bool kRemap>
 struct PairCfg {
   static constexpr bool kTma = pair_tma(EPI, kRemap);
+  // (16 epilogue warps with one box each measured slower than 8 with two: register spills)
   static constexpr int kWarps = pair_epi_warps(EPI, kRemap);
+  static constexpr int kBufs = 2;  // staging boxes per epilogue warp
   static constexpr int kThreads = 128 + 32 * kWarps;
   static constexpr int kABytes = 128 * kBK * 2;
   static constexpr int kBBytes = 128 * kBK * 2;  // this CTA's half of the 256-row W tile
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kEpiBytes = kTma ? kWarps * 2 * 4096 : kEpiWarps * 32 * 32 * 4;
+  static constexpr int kEpiBytes = kTma ? kWarps * kBufs * 4096 : kEpiWarps * 32 * 32 * 4;
   static constexpr int kStages = kEpiBytes > 32768 ? 5 : 6;
   static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 256;
 };
@@ -559,6 +559,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
         constexpr int NCH = (BN / kSplit) / CW;
         const long long m = m_base + lane;
         const bool row_ok = m < M;
+        // LN finish (EPI_LN_*): this thread's row statistics, once per tile
+        float ln_mu = 0.f, ln_rstd = 0.f;
+        if constexpr (epi_is_ln(EPI)) {
+          if (row_ok) {
+            const float2 st = __ldg(reinterpret_cast<const float2*>(epi.ln_stats) + m);
+            ln_mu = st.x * epi.inv_dim;
+            ln_rstd = rsqrtf(fmaxf(st.y * epi.inv_dim - ln_mu * ln_mu, 0.f) + 1e-6f);
+          }
+        }
+        // row statistics of the stored values (EPI_*_STATS) and this row's output row index
+        float st_s = 0.f, st_q = 0.f;
+        long long orow = m;
+        if constexpr (kRemap) {
+          const long long bm = m / epi.rows_in;
+          orow = bm * epi.rows_out + epi.row_off + (m - bm * epi.rows_in);
+        }
 #pragma unroll 1
         for (int c = 0; c < NCH; ++c) {
           const int n0 = n_blk * BN + col0 + c * CW;
@@ -596,21 +612,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
               }
             }
           }
-          const float4* bp = reinterpret_cast<const float4*>(epi.bias + n0);
+          if constexpr (epi_is_ln(EPI)) {
+            const float4* c1p = reinterpret_cast<const float4*>(epi.c1 + n0);
+            const float4* c2p = reinterpret_cast<const float4*>(epi.c2 + n0);
 #pragma unroll
-          for (int j = 0; j < CW / 4; ++j) {
-            const float4 b = __ldg(bp + j);
-            v[4 * j] += b.x;
-            v[4 * j + 1] += b.y;
-            v[4 * j + 2] += b.z;
-            v[4 * j + 3] += b.w;
+            for (int j = 0; j < CW / 4; ++j) {
+              const float4 a1 = __ldg(c1p + j), a2 = __ldg(c2p + j);
+              v[4 * j] = fmaf(ln_rstd, fmaf(-ln_mu, a1.x, v[4 * j]), a2.x);
+              v[4 * j + 1] = fmaf(ln_rstd, fmaf(-ln_mu, a1.y, v[4 * j + 1]), a2.y);
+              v[4 * j + 2] = fmaf(ln_rstd, fmaf(-ln_mu, a1.z, v[4 * j + 2]), a2.z);
+              v[4 * j + 3] = fmaf(ln_rstd, fmaf(-ln_mu, a1.w, v[4 * j + 3]), a2.w);
+            }
+          } else {
+            const float4* bp = reinterpret_cast<const float4*>(epi.bias + n0);
+#pragma unroll
+            for (int j = 0; j < CW / 4; ++j) {
+              const float4 b = __ldg(bp + j);
+              v[4 * j] += b.x;
+              v[4 * j + 1] += b.y;
+              v[4 * j + 2] += b.z;
+              v[4 * j + 3] += b.w;
+            }
           }
           if constexpr (epi_is_gelu(EPI)) {
 #pragma unroll
             for (int j = 0; j < CW; ++j) v[j] = gelu_erf_fast(v[j]);
           }
-          uint8_t* sbuf = epi_smem + (ew * 2 + tma_buf) * 4096;
-          if (lane == 0) bulk_wait_group_read<1>();  // the store that last used sbuf has read it
+          if constexpr (epi_is_stats(EPI)) {
+            // bf16 copy of the stored row chunk (next GEMM's A operand) + row statistics
+            if (row_ok) {
+              uint4* xr = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.xh) + orow * N + n0);
+#pragma unroll
+              for (int j = 0; j < CW / 8; ++j)
+                xr[j] = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                                   pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+#pragma unroll
+              for (int j = 0; j < CW; ++j) {
+                st_s += v[j];
+                st_q = fmaf(v[j], v[j], st_q);
+              }
+            }
+          }
+          uint8_t* sbuf = epi_smem + (ew * Cfg::kBufs + tma_buf) * 4096;
+          if (lane == 0) bulk_wait_group_read<Cfg::kBufs - 1>();  // last store from sbuf has read it
           __syncwarp();
           const uint32_t srow = smem_u32(sbuf) + lane * 128;
           // Row remap: a row of this box that belongs to the next image is also stored
@@ -654,7 +698,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
             }
             bulk_commit_group();
           }
-          tma_buf ^= 1;
+          tma_buf = (tma_buf + 1) % Cfg::kBufs;
+        }
+        if constexpr (epi_is_stats(EPI)) {
+          if (row_ok && !epi.skip) {
+            atomicAdd(epi.stats + 2 * orow, st_s);
+            atomicAdd(epi.stats + 2 * orow + 1, st_q);
+          }
         }
       } else {
         uint32_t r0[32], r1[32];
