@@ -47,6 +47,7 @@ struct AttnTcLayout {
   int n_qt;     // ceil(t / 128)
   int n_kv;     // K/V ring slots (2 when t_pad <= 256)
   int n_s;      // TMEM S slots (2 when t_pad <= 256)
+  int rowsplit; // 1: softmax group g owns every other tile (t_pad <= 128); 0: groups split keys
   uint32_t kv_bytes;  // per slot: K then V
   uint32_t kv_off, p_off, bias_off, red_off, bar_off, smem_bytes;
 };
@@ -58,6 +59,7 @@ AttnTcLayout attn_layout(int t) {
   L.n_qt = (t + kQTile - 1) / kQTile;
   L.n_kv = L.t_pad <= 256 ? 2 : 1;
   L.n_s = L.t_pad <= 256 ? 2 : 1;
+  L.rowsplit = L.t_pad <= 128;  // measured: faster for short rows, key split wins at t ~ 197
   L.kv_bytes = 2u * L.n_kb * kBlkBytes;
   uint32_t off = kQBytes;  // Q: one slot (Q(n+1) is only needed after S(n) has long completed)
   L.kv_off = off;
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&q_full[s], 1);
       mbar_init(&q_free[s], 1);
       mbar_init(&s_full[s], 1);
-      mbar_init(&s_free[s], 256);
+      mbar_init(&s_free[s], L.rowsplit ? 128 : 256);  // row-split: one group reads a slot
       mbar_init(&o_full[s], 1);
     }
     for (int s = 0; s < 4; ++s) {
@@ -188,6 +190,63 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(&o_full[sslot]);
         if (last_of_item) umma_commit(&kv_free[kvs]);
       };
+      if (L.rowsplit) {
+        // Row-split mode (t_pad <= 128): tile n lives in S slot n % 2 and is softmaxed by group
+        // n % 2.  Non-blocking scheduler: issue whichever is ready first, the next S (at most two
+        // tiles in flight) or the next PV block, so one group never waits on the other.
+        const int n_my = n_items > static_cast<int>(blockIdx.x)
+                             ? (n_items - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
+                             : 0;
+        const int T = n_my * L.n_qt;
+        int sN = 0, pN = 0, pkb = 0;
+        while (pN < T) {
+          if (sN < T && sN < pN + 2) {
+            const int it = sN / L.n_qt, qt = sN - it * L.n_qt;
+            const int slot = sN & 1;
+            const int kvs = it % L.n_kv;
+            if (mbar_test(&s_free[slot], ((sN >> 1) & 1) ^ 1) && mbar_test(&q_full[0], sN & 1) &&
+                (qt != 0 || mbar_test(&kv_full[kvs], (it / L.n_kv) & 1))) {
+              tc_fence_after();
+              const uint8_t* sK = sKV + kvs * L.kv_bytes;
+              const uint64_t qdesc = umma_desc_sw128(smem_u32(sQ));
+              const uint32_t idesc_s = idesc_bf16(kQTile, L.t_pad);
+              const uint64_t kdesc = umma_desc_sw128(smem_u32(sK));
+#pragma unroll
+              for (int k = 0; k < kHd / 16; ++k)
+                umma_f16(tmem + slot * 256, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0);
+              umma_commit(&s_full[slot]);
+              umma_commit(&q_free[0]);
+              ++sN;
+            }
+          }
+          if (pN < sN) {
+            const int grp = pN & 1;
+            const uint32_t u = p_use[grp];
+            const int ps = 2 * grp + (u & 1);
+            if (mbar_test(&p_full[ps], (u >> 1) & 1)) {
+              ++p_use[grp];
+              tc_fence_after();
+              const int it = pN / L.n_qt, qt = pN - it * L.n_qt;
+              const int kvs = it % L.n_kv;
+              const uint8_t* sV = sKV + kvs * L.kv_bytes + L.n_kb * kBlkBytes;
+              const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
+              const uint32_t vbase = smem_u32(sV + pkb * kBlkBytes);
+#pragma unroll
+              for (int kc = 0; kc < kKeyBlk / 16; ++kc) {
+                const uint64_t vdesc = umma_desc_sw128_mn(vbase + kc * 2048, 8192, 1024);
+                umma_f16(tmem + grp * 256, pdesc + 2 * kc, vdesc, idesc_pv, (pkb | kc) != 0);
+              }
+              umma_commit(&p_free[ps]);
+              if (++pkb == L.n_kb) {
+                umma_commit(&o_full[grp]);
+                if (qt + 1 == L.n_qt) umma_commit(&kv_free[kvs]);
+                ++pN;
+                pkb = 0;
+              }
+            }
+          }
+        }
+      } else {
       uint32_t it = 0, qcnt = 0, tcnt = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
         const int kvs = it % L.n_kv;
@@ -221,6 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (pend_slot >= 0) issue_pv(pend_slot, pend_kvs, pend_last);
+      }
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
@@ -344,6 +404,119 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
 
+    if (L.rowsplit) {
+      // ---- row-split: group g owns the tiles of S slot g (every other tile); no cross-group
+      // exchange, bias kept per group.
+      const uint32_t s_bias_g = s_bias + g * 256 * 4;
+      const uint32_t la = lane_base + g * 256;
+      uint32_t k = 0;  // tiles processed by this group
+      uint32_t tile = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int b = item / H, h = item - b * H;
+        const int row_base = b * t;
+        bool have_bias = false;
+        for (int qt = 0; qt < L.n_qt; ++qt, ++tile) {
+          if (static_cast<int>(tile & 1) != g) continue;
+          if (!have_bias) {
+            named_bar_sync(2 + g, 128);  // group done with the previous item's bias
+            for (int j = i; j < L.t_pad; j += 128)
+              sts_f32(s_bias_g + j * 4,
+                      j < t ? (size != nullptr ? size[static_cast<long long>(row_base) + j] : 1.f) : 0.f);
+            named_bar_sync(2 + g, 128);
+            have_bias = true;
+          }
+          mbar_wait(&s_full[g], k & 1);
+          tc_fence_after();
+          // pass 1: row max of the raw scores over the valid keys
+          float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+          for (int kb = 0; kb < L.n_kb; ++kb) {
+            uint32_t r[64];
+            tmem_ld_32x32b_x32(la + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+            tmem_ld_32x32b_x32(la + kb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+            tmem_ld_wait();
+            if ((kb + 1) * 64 <= t) {
+#pragma unroll
+              for (int j = 0; j < 64; j += 4) {
+                m4[0] = fmaxf(m4[0], __uint_as_float(r[j]));
+                m4[1] = fmaxf(m4[1], __uint_as_float(r[j + 1]));
+                m4[2] = fmaxf(m4[2], __uint_as_float(r[j + 2]));
+                m4[3] = fmaxf(m4[3], __uint_as_float(r[j + 3]));
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 64; ++j)
+                if (kb * 64 + j < t) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(r[j]));
+            }
+          }
+          const float nmx = -fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
+          // pass 2: P blocks
+          float s4[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int kb = 0; kb < L.n_kb; ++kb, ++use) {
+            uint32_t r[64];
+            tmem_ld_32x32b_x32(la + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+            tmem_ld_32x32b_x32(la + kb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+            const int pst = 2 * g + (use & 1);
+            const uint32_t s_prow = s_prow0 + (use & 1) * kPBytes;
+            mbar_wait(&p_free[pst], ((use >> 1) & 1) ^ 1);
+            tmem_ld_wait();
+            const bool weighted = kHasSize || (kb + 1) * 64 > t;
+#pragma unroll
+            for (int chunk = 0; chunk < 8; ++chunk) {
+              const uint32_t* rr = &r[chunk * 8];
+              float p[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) p[e] = ex2_approx(fmaf(__uint_as_float(rr[e]), scale_log2, nmx));
+              if (weighted) {
+                const float4 w0 = lds_f4(s_bias_g + (kb * 64 + chunk * 8) * 4);
+                const float4 w1 = lds_f4(s_bias_g + (kb * 64 + chunk * 8 + 4) * 4);
+                p[0] *= w0.x;
+                p[1] *= w0.y;
+                p[2] *= w0.z;
+                p[3] *= w0.w;
+                p[4] *= w1.x;
+                p[5] *= w1.y;
+                p[6] *= w1.z;
+                p[7] *= w1.w;
+              }
+              s4[0] += p[0] + p[4];
+              s4[1] += p[1] + p[5];
+              s4[2] += p[2] + p[6];
+              s4[3] += p[3] + p[7];
+              sts_u4(s_prow + ((chunk ^ (i & 7)) << 4),
+                     make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]),
+                                pack_bf16(p[6], p[7])));
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();  // S reads done before the PV MMA may overwrite block 0
+            mbar_arrive(&p_full[pst]);
+          }
+          const float inv = rcp_approx((s4[0] + s4[1]) + (s4[2] + s4[3]));
+          // epilogue: O (64 columns of this slot) / sum -> bf16 row
+          mbar_wait(&o_full[g], k & 1);
+          tc_fence_after();
+          uint32_t o0[32], o1[32];
+          tmem_ld_32x32b_x32(la, o0);
+          tmem_ld_32x32b_x32(la + 32, o1);
+          tmem_ld_wait();
+          tc_fence_before();
+          mbar_arrive(&s_free[g]);
+          const int q = qt * kQTile + i;
+          if (q < t) {
+            uint4* orow = reinterpret_cast<uint4*>(out + (static_cast<long long>(row_base) + q) * D + h * kHd);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint32_t* oo = c < 4 ? &o0[8 * c] : &o1[8 * (c - 4)];
+              orow[c] = make_uint4(
+                  pack_bf16(__uint_as_float(oo[0]) * inv, __uint_as_float(oo[1]) * inv),
+                  pack_bf16(__uint_as_float(oo[2]) * inv, __uint_as_float(oo[3]) * inv),
+                  pack_bf16(__uint_as_float(oo[4]) * inv, __uint_as_float(oo[5]) * inv),
+                  pack_bf16(__uint_as_float(oo[6]) * inv, __uint_as_float(oo[7]) * inv));
+            }
+          }
+          ++k;
+        }
+      }
+    } else {
     // deferred epilogue of the previous tile (two-slot mode)
     bool pend = false;
     uint32_t pend_t = 0;
@@ -397,6 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (pend) epilogue(pend_t, pend_row, pend_h, pend_qt, pend_inv);
+    }
   }
   grid_dep_launch();
   tc_fence_before();
