@@ -106,3 +106,32 @@ def test_vit_b16_bf16_sweep_gammas(gamma):
     fr, rf = _finite(forced), _finite(ref)
     scale = rf.abs().max().item()
     assert (fr - rf).abs().max().item() <= BF16_TOL * scale
+
+
+@pytest.mark.parametrize("gamma", [-16, 0, 16])
+def test_vit_l16_config3_bf16(gamma):
+    """Config 3 shapes (ViT-L/16; gamma=+16 reaches t=581 -> mma.sync attention fallback),
+    batch 2, index-forced bf16 vs the oracle."""
+    cfg, ref, tr, out, gtr, forced, _ = _run("vit_l16", gamma, 2, "bf16")
+    fr, rf = _finite(forced), _finite(ref)
+    assert (fr - rf).abs().max().item() <= BF16_TOL * rf.abs().max().item()
+
+
+def test_vit_l16_fp32_merge_indices():
+    """ViT-L/16 gamma=-16 in fp32 mode: merge index sets bit-exact, logits rtol 1e-4."""
+    cfg, ref, tr, out, gtr, _, _ = _run("vit_l16", -16, 2, "fp32")
+    _assert_indices_equal(tr, gtr)
+    scale = _finite(ref).abs().max().item()
+    torch.testing.assert_close(_finite(out), _finite(ref), rtol=1e-4, atol=1e-4 * scale)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_vit_h14_config5(dtype):
+    """Config 5 shapes (ViT-H/14: P=14 -> K=588 padded to 640, head dim 80, D=1280), gamma=-24."""
+    cfg, ref, tr, out, gtr, forced, _ = _run("vit_h14", -24, 2, dtype)
+    scale = _finite(ref).abs().max().item()
+    if dtype == "fp32":
+        _assert_indices_equal(tr, gtr)
+        torch.testing.assert_close(_finite(out), _finite(ref), rtol=1e-4, atol=1e-4 * scale)
+    else:
+        assert (_finite(forced) - _finite(ref)).abs().max().item() <= BF16_TOL * scale
