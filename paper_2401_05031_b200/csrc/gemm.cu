@@ -575,8 +575,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           const long long bm = m / epi.rows_in;
           orow = bm * epi.rows_out + epi.row_off + (m - bm * epi.rows_in);
         }
-#pragma unroll 1
-        for (int c = 0; c < NCH; ++c) {
+        // compute(c): TMEM columns of box c -> bias / LN / GELU / residual -> 8 packed 16-byte
+        // words of this thread's row (w); stage_store(c, w): swizzled staging box + TMA store.
+        auto compute = [&](int c, uint4 (&w)[8]) -> bool {
           const int n0 = n_blk * BN + col0 + c * CW;
           float v[CW];
           {
@@ -588,12 +589,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
 #pragma unroll
             for (int j = 0; j < CW; ++j) v[j] = __uint_as_float(r[j]);
           }
-          if (c + 1 == NCH) {
+          if (c + 1 == NCH) {  // accumulator fully read: hand it back to the MMA warp
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
           }
-          if (epi.skip) continue;
+          if (epi.skip == 1) return false;
           if constexpr (epi_is_resid(EPI) || epi_is_patch(EPI)) {
             if (row_ok) {
               const float4* rp =
@@ -627,7 +628,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
             const float4* bp = reinterpret_cast<const float4*>(epi.bias + n0);
 #pragma unroll
             for (int j = 0; j < CW / 4; ++j) {
-              const float4 b = __ldg(bp + j);
+              const float4 b = epi.skip == 3 ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(bp + j);
               v[4 * j] += b.x;
               v[4 * j + 1] += b.y;
               v[4 * j + 2] += b.z;
@@ -653,13 +654,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
               }
             }
           }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if constexpr (sizeof(OutT) == 2) {
+              w[j] = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                                pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+            } else {
+              w[j] = make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                                __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+            }
+          }
+          return true;
+        };
+        auto stage_store = [&](int c, const uint4 (&w)[8]) {
+          const int n0 = n_blk * BN + col0 + c * CW;
           uint8_t* sbuf = epi_smem + (ew * Cfg::kBufs + tma_buf) * 4096;
           if (lane == 0) bulk_wait_group_read<Cfg::kBufs - 1>();  // last store from sbuf has read it
           __syncwarp();
           const uint32_t srow = smem_u32(sbuf) + lane * 128;
-          // Row remap: a row of this box that belongs to the next image is also stored
-          // directly (the box's TMA store lands it in this image's prompt / padding slots,
-          // which insert_rows rewrites, or clips it past rows_out).
+          // Row remap: a row of this box that belongs to a later image is also stored directly
+          // (the box's TMA store lands it in this image's prompt / padding slots, which
+          // insert_rows rewrites, or clips it past rows_out).
           uint4* spill_row = nullptr;
           if constexpr (kRemap) {
             const int b = static_cast<int>(m_base / epi.rows_in);
@@ -674,20 +689,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           }
 #pragma unroll
           for (int j = 0; j < 8; ++j) {  // 16-byte chunk j of this row, SW128 position j ^ (row & 7)
-            uint4 w;
-            if constexpr (sizeof(OutT) == 2) {
-              w = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
-                             pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
-            } else {
-              w = make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
-                             __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
-            }
-            sts_u4(srow + ((j ^ (lane & 7)) << 4), w);
-            if (kRemap && spill_row != nullptr) spill_row[j] = w;
+            sts_u4(srow + ((j ^ (lane & 7)) << 4), w[j]);
+            if (kRemap && spill_row != nullptr) spill_row[j] = w[j];
           }
           fence_proxy_async_shared();
           __syncwarp();
-          if (lane == 0) {
+          if (lane == 0 && epi.skip != 2) {
             if constexpr (kRemap) {
               // 3D view [B][rows_out][N]: the box goes to image b at its in-image row.
               const int b = static_cast<int>(m_base / epi.rows_in);
@@ -699,6 +706,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
             bulk_commit_group();
           }
           tma_buf = (tma_buf + 1) % Cfg::kBufs;
+        };
+        // (Interleaved per box.  Reading every box and releasing the accumulator before any
+        // staging wait measured slower: the extra live registers cost more than the wait.)
+#pragma unroll 1
+        for (int c = 0; c < NCH; ++c) {
+          uint4 w[8];
+          if (compute(c, w)) stage_store(c, w);
         }
         if constexpr (epi_is_stats(EPI)) {
           if (row_ok && !epi.skip) {
@@ -1023,8 +1037,9 @@ static int dispatch_bf16(const CUtensorMap& a, const CUtensorMap& b, int M, int 
 int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, bool out_bf16,
               const GemmEpi& epi_in, cudaStream_t stream) {
   static const int skip_epi = [] {
-    const char* v = getenv("TA_GEMM_SKIP_EPILOGUE");  // profiling only: mainloop without epilogue
-    return v && v[0] == '1';
+    // profiling only: 1 = mainloop + TMEM drain only, 2 = no TMA store, 3 = no bias loads
+    const char* v = getenv("TA_GEMM_SKIP_EPILOGUE");
+    return v ? atoi(v) : 0;
   }();
   GemmEpi epi = epi_in;
   epi.skip = skip_epi;

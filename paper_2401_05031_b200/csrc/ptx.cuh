@@ -118,9 +118,12 @@ __device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+// Arrive on a barrier in another CTA of the cluster (address from mapa_shared).  Default
+// semantics (release, cta scope) as CUTLASS's ClusterBarrier::arrive(cta_id): the explicit
+// .release.cluster form compiles to MEMBAR.ALL.GPU, which stalled the GEMM epilogue warps.
+// Ordering of the preceding tcgen05.ld is provided by tcgen05.fence::before_thread_sync.
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
