@@ -81,6 +81,8 @@ __global__ void __launch_bounds__(128)
 
   grid_dep_wait();
 
+  grid_dep_launch();  // early trigger: the next kernel's prologue overlaps our tail
+
   auto load_kv = [&](int buf, int k0) {
     for (int i = threadIdx.x; i < C::kBK * C::kChunks; i += blockDim.x) {
       const int row = i / C::kChunks, ch = i % C::kChunks;
@@ -235,7 +237,6 @@ __global__ void __launch_bounds__(128)
           pack_bf16(o[dc][2 * half] * inv, o[dc][2 * half + 1] * inv);
     }
   }
-  grid_dep_launch();
 }
 
 // fp32 SIMT: one thread per query row, keys/values through smem in blocks of 32.

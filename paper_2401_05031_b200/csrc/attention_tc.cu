@@ -135,6 +135,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   grid_dep_wait();  // qkv is the previous kernel's output
 
+  grid_dep_launch();  // early trigger: the next kernel's prologue overlaps our tail
+
   if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
@@ -572,7 +574,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (pend) epilogue(pend_t, pend_row, pend_h, pend_qt, pend_inv);
     }
   }
-  grid_dep_launch();
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {

@@ -256,6 +256,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
 
   // Inputs (A) may be produced by the previous kernel in the stream (PDL).
   grid_dep_wait();
+  grid_dep_launch();  // early trigger: the next kernel's prologue overlaps our tail
 
   const int num_m = (M + kBM - 1) / kBM;
   const int num_n = N / BN;
@@ -380,7 +381,6 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
       }
     }
   }
-  grid_dep_launch();
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -464,6 +464,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
   const uint32_t tmem_base = *tmem_slot;
 
   grid_dep_wait();
+
+  grid_dep_launch();  // early trigger: the next kernel's prologue overlaps our tail
 
   const int num_m = (M + 255) / 256;
   const int num_n = N / BN;
@@ -763,7 +765,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
   if constexpr (Cfg::kTma) {
     if (warp >= 4 && lane == 0) bulk_wait_group<0>();  // staged boxes fully stored
   }
-  grid_dep_launch();
   tc_fence_before();
   cluster_sync();
   if (warp == 2) {

@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(256)
   const int na = (t + 1) / 2, nb = t / 2;
   float* base = scratch + static_cast<long long>(b) * 4 * kRows * cp;
   grid_dep_wait();
+  grid_dep_launch();  // early trigger: the next kernel's prologue overlaps our tail
   const int lane = lane_id();
   const int row = blockIdx.y * 32 + warp_id() * 4;
   for (int rr = row; rr < row + 4; ++rr) {
@@ -106,7 +107,6 @@ __global__ void __launch_bounds__(256)
       }
     }
   }
-  grid_dep_launch();
 }
 
 __global__ void __launch_bounds__(128, 1)
@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   grid_dep_wait();  // scratch comes from metric_split_kernel
+  grid_dep_launch();  // early trigger: the next kernel's prologue overlaps our tail
 
   if (i == 0) {
     mbar_arrive_expect_tx(bar_ld, 4 * tile_bytes);
@@ -214,7 +215,6 @@ __global__ void __launch_bounds__(128, 1)
       unm_out[static_cast<long long>(b) * (na - r) + pos] = i;
     }
   }
-  grid_dep_launch();
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();

@@ -134,6 +134,7 @@ __global__ void layernorm_kernel(const float* __restrict__ x, const float* __res
                                  const float* __restrict__ bvec, T* __restrict__ out, int rows) {
   constexpr int D = 128 * VEC;
   grid_dep_wait();
+  grid_dep_launch();  // early trigger: the next kernel's prologue overlaps our tail
   const int row = blockIdx.x * (blockDim.x / 32) + warp_id();
   if (row < rows) {
     const int lane = lane_id();
@@ -173,7 +174,6 @@ __global__ void layernorm_kernel(const float* __restrict__ x, const float* __res
       }
     }
   }
-  grid_dep_launch();
 }
 
 template <typename T>

@@ -39,6 +39,8 @@ __global__ void __launch_bounds__(kMatchThreads)
   const int warp = warp_id(), lane = lane_id(), nwarps = blockDim.x / 32;
 
   grid_dep_wait();
+
+  grid_dep_launch();  // early trigger: the next kernel's prologue overlaps our tail
   // 1) metric rows (mean over heads, fixed head order), then L2-normalise (x / ||x||).
   for (int row = warp; row < t; row += nwarps) {
     float* dstrow = (row & 1) ? Bs + (row >> 1) * cs : As + (row >> 1) * cs;
@@ -121,7 +123,6 @@ __global__ void __launch_bounds__(kMatchThreads)
       unmb[pos] = i;
     }
   }
-  grid_dep_launch();
 }
 
 static int match_backend() {
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(256)
   const int n_unm = na - r;
   const int tp = t - r;
   grid_dep_wait();
+  grid_dep_launch();  // early trigger: the next kernel's prologue overlaps our tail
   for (int i = threadIdx.x; i < r; i += blockDim.x) {
     s_src[i] = src[static_cast<long long>(b) * r + i];
     s_dst[i] = dst[static_cast<long long>(b) * r + i];
@@ -297,7 +299,6 @@ __global__ void __launch_bounds__(256)
       }
     }
   }
-  grid_dep_launch();
 }
 
 template <typename T>
