@@ -10,6 +10,9 @@
 // The per-layer token count t_l is static per (model, gamma); all buffers live in the
 // caller's workspace, so the whole call is CUDA-graph capturable.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -166,6 +169,47 @@ size_t trace_len(const Schedule& s, int B) {
     if (_rc != TA_OK) return _rc; \
   } while (0)
 
+// Profiling only (TA_PROFILE_STAGES=1, never inside a graph): CUDA events around every
+// stage of ta_forward, summed per stage name and printed after the forward.
+namespace {
+struct StageProfiler {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  std::vector<std::pair<const char*, cudaEvent_t>> marks;
+  explicit StageProfiler(cudaStream_t s) : st(s) {
+    const char* v = getenv("TA_PROFILE_STAGES");
+    on = v && v[0] == '1';
+    mark("start");
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    marks.emplace_back(name, e);
+  }
+  ~StageProfiler() {
+    if (!on || marks.size() < 2) return;
+    cudaEventSynchronize(marks.back().second);
+    std::map<std::string, std::pair<int, float>> agg;
+    float total = 0.f;
+    for (size_t i = 1; i < marks.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
+      auto& a = agg[marks[i].first];
+      a.first += 1;
+      a.second += ms;
+      total += ms;
+    }
+    for (auto& kv : agg)
+      fprintf(stderr, "[ta stage] %-14s n=%3d %9.1f us\n", kv.first.c_str(), kv.second.first,
+              kv.second.second * 1e3f);
+    fprintf(stderr, "[ta stage] total %9.1f us\n", total * 1e3f);
+    for (auto& m : marks) cudaEventDestroy(m.second);
+  }
+};
+}  // namespace
+
 extern "C" {
 #pragma GCC visibility push(default)
 
@@ -321,6 +365,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
   Workspace w = carve(m, B, s, static_cast<char*>(ws));
   if (ws_bytes < w.total) return TA_ERR_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  StageProfiler prof(st);
   const ta_model_desc& d = m->d;
   const int D = d.dim, L = d.depth, N = m->n_tokens;
   const int act = d.dtype;
@@ -337,6 +382,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
 
   // ---- patch embedding + cls + layer-0 prompts
   TA_TRY(patchify(images, w.patches, B, d.img, d.patch, m->kp, act, st));
+  prof.mark("patchify");
   {
     GemmEpi e;
     e.bias = static_cast<const float*>(m->w.patch_b);
@@ -352,11 +398,13 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
     }
     TA_TRY(linear(m, w.patches, m->w.patch_w, B * m->n_patches, D, m->kp,
                   fused ? EPI_PATCH_STATS : EPI_PATCH, e, st));
+  prof.mark("patch_gemm");
   }
   TA_TRY(insert_rows(w.x[0], B, s.t[0], D, static_cast<const float*>(m->w.cls),
                      static_cast<const float*>(m->w.pos), ptab, task_ids, 0,
                      gamma > 0 ? gamma : 0, N, st, fused ? w.h : nullptr,
                      fused ? ln1_stats : nullptr));
+  prof.mark("insert_rows");
 
   int cur = 0;
   const float* size = nullptr;
@@ -370,6 +418,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
       TA_TRY(insert_rows(w.x[cur], B, t, D, nullptr, nullptr, ptab, task_ids, l, gamma,
                          accumulate ? t - gamma : N, st, fused ? w.h : nullptr,
                          fused ? ln1_stats : nullptr));
+  prof.mark("insert_rows");
     const int M = B * t;
     {  // LN1 + QKV
       GemmEpi e;
@@ -380,14 +429,18 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         e.c2 = static_cast<const float*>(Lw.qkv_c2);
         e.inv_dim = 1.0f / D;
         TA_TRY(linear(m, w.h, Lw.qkv_w_ln, M, 3 * D, D, EPI_LN_BIAS, e, st));
+  prof.mark("qkv");
       } else {
         TA_TRY(layernorm(w.x[cur], static_cast<const float*>(Lw.ln1_w),
                          static_cast<const float*>(Lw.ln1_b), w.h, M, D, act, st));
+  prof.mark("ln1");
         e.bias = static_cast<const float*>(Lw.qkv_b);
         TA_TRY(linear(m, w.h, Lw.qkv_w, M, 3 * D, D, EPI_BIAS, e, st));
+  prof.mark("qkv");
       }
     }
     TA_TRY(attention(w.qkv, size, B, t, d.heads, m->hd, w.attn, act, st));
+  prof.mark("attention");
     const int r = s.r[l];
     {  // proj + residual (+ LN2 stats when no merge follows)
       GemmEpi e;
@@ -399,8 +452,10 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         e.xh = w.h;
         e.stats = ln2_stats;
         TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID_STATS, e, st));
+  prof.mark("proj");
       } else {
         TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID, e, st));
+  prof.mark("proj");
       }
     }
     int tp = t;
@@ -421,9 +476,11 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         cudaMemcpyAsync(merge_trace + (src - forced_trace), src,
                         sizeof(int32_t) * static_cast<size_t>(B) * (2 * r + na - r),
                         cudaMemcpyDeviceToDevice, st);
+      prof.mark("match");
       TA_TRY(merge(w.x[cur], size, B, t, D, r, src, dst, unm, static_cast<const float*>(Lw.ln2_w),
                    static_cast<const float*>(Lw.ln2_b), w.x[cur ^ 1], w.size[size_buf], w.h, act,
                    st, fused ? ln2_stats : nullptr));
+  prof.mark("merge");
       cur ^= 1;
       size = w.size[size_buf];
       size_buf ^= 1;
@@ -431,6 +488,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
     } else if (!fused) {
       TA_TRY(layernorm(w.x[cur], static_cast<const float*>(Lw.ln2_w),
                        static_cast<const float*>(Lw.ln2_b), w.h, M, D, act, st));
+  prof.mark("ln2");
     }
     const int Mp = B * tp;
     {  // LN2 + fc1 + GELU
@@ -442,9 +500,11 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         e.c2 = static_cast<const float*>(Lw.fc1_c2);
         e.inv_dim = 1.0f / D;
         TA_TRY(linear(m, w.h, Lw.fc1_w_ln, Mp, d.mlp_dim, D, EPI_LN_GELU, e, st));
+  prof.mark("fc1");
       } else {
         e.bias = static_cast<const float*>(Lw.fc1_b);
         TA_TRY(linear(m, w.h, Lw.fc1_w, Mp, d.mlp_dim, D, EPI_BIAS_GELU, e, st));
+  prof.mark("fc1");
       }
     }
     {  // fc2 + residual (+ next layer's LN1 stats)
@@ -469,6 +529,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
       }
       TA_TRY(linear(m, w.mlp, Lw.fc2_w, Mp, D, d.mlp_dim,
                     stats ? EPI_BIAS_RESID_STATS : EPI_BIAS_RESID, e, st));
+  prof.mark("fc2");
       if (restride) cur ^= 1;
     }
     t = tp;
@@ -476,6 +537,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
   TA_TRY(head(w.x[cur], B, t, D, static_cast<const float*>(m->w.norm_w),
               static_cast<const float*>(m->w.norm_b), m->heads_dev, task_ids, logits,
               d.max_classes, st));
+  prof.mark("head");
   return TA_OK;
 }
 
