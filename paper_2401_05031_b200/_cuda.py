@@ -16,7 +16,7 @@ from .errors import ConfigError, ProfileGapError
 __all__ = ["lib", "check", "LIB_PATH", "ModelDesc", "LayerWeights", "Weights", "TAError",
            "DTYPE_BF16", "DTYPE_F32", "PROMPT_ACCUMULATE", "PROMPT_REPLACE", "EXPORTED_SYMBOLS"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtokadapt_cuda.so")
+LIB_PATH = os.environ.get("TA_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtokadapt_cuda.so")
 
 TA_OK, TA_ERR_INVALID, TA_ERR_SHAPE, TA_ERR_CONFIG, TA_ERR_NO_PROMPT = 0, -1, -2, -3, -4
 TA_ERR_NO_WEIGHTS, TA_ERR_WORKSPACE, TA_ERR_CUDA, TA_ERR_ARCH = -5, -6, -7, -8

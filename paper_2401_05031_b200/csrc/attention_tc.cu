@@ -29,6 +29,8 @@ namespace ta {
 
 int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                       uint32_t box_rows);
+int make_tmap_attn_out(CUtensorMap* map, const void* base, uint64_t images, uint64_t t,
+                       uint64_t cols);
 
 namespace {
 
@@ -83,9 +85,96 @@ __device__ __forceinline__ void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+// Exponentials per 8-key chunk evaluated by exp2_poly2 on the FMA pipe (in pairs) for even /
+// odd chunks; the rest go to the SFU.  The SFU issues 16 ex2/clk/SM against 128 FMA lanes,
+// so with ~4.5 other instructions per key an all-SFU softmax is SFU-bound; 3 of 8 on the
+// FMA pipe balances the two (measured in tools/attn_bench.py).
+#ifndef TA_ATTN_POLY_EVEN
+#define TA_ATTN_POLY_EVEN 1
+#endif
+#ifndef TA_ATTN_POLY_ODD
+#define TA_ATTN_POLY_ODD 2
+#endif
+
+// p = w * 2^(s * scale_log2 - m) for 8 keys of one query row; accumulates the fp32 row sum
+// into acc (two packed pairs) and returns the bf16 P chunk.
+template <int kPolyPairs>
+__device__ __forceinline__ uint4 softmax_chunk8(const uint32_t* rr, uint64_t sc2, uint64_t nm2,
+                                                bool weighted, uint32_t s_w, uint64_t (&acc)[2]) {
+  uint64_t p[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint64_t x = ffma2(f2_pack(__uint_as_float(rr[2 * e]), __uint_as_float(rr[2 * e + 1])), sc2, nm2);
+#ifdef TA_ATTN_EXP_NONE  // profiling only: wrong results
+    if (true) {
+      p[e] = x;
+#else
+    if (e >= 4 - kPolyPairs) {
+      p[e] = exp2_poly2(x);
+#endif
+    } else {
+      const float2 v = f2_unpack(x);
+      p[e] = f2_pack(ex2_approx(v.x), ex2_approx(v.y));
+    }
+  }
+  if (weighted) {
+    const float4 w0 = lds_f4(s_w);
+    const float4 w1 = lds_f4(s_w + 16);
+    p[0] = fmul2(p[0], f2_pack(w0.x, w0.y));
+    p[1] = fmul2(p[1], f2_pack(w0.z, w0.w));
+    p[2] = fmul2(p[2], f2_pack(w1.x, w1.y));
+    p[3] = fmul2(p[3], f2_pack(w1.z, w1.w));
+  }
+  acc[0] = fadd2(acc[0], p[0]);
+  acc[1] = fadd2(acc[1], p[1]);
+  acc[0] = fadd2(acc[0], p[2]);
+  acc[1] = fadd2(acc[1], p[3]);
+  const float2 a = f2_unpack(p[0]), b = f2_unpack(p[1]), c = f2_unpack(p[2]), d = f2_unpack(p[3]);
+  return make_uint4(pack_bf16(a.x, a.y), pack_bf16(b.x, b.y), pack_bf16(c.x, c.y), pack_bf16(d.x, d.y));
+}
+
+// 64 keys (one P block row): chunk c -> 16-byte swizzled slot (c ^ (row & 7)) of the row.
+__device__ __forceinline__ void softmax_block64(const uint32_t (&r)[64], uint64_t sc2, uint64_t nm2,
+                                                bool weighted, uint32_t s_w, uint32_t s_prow,
+                                                int row, uint64_t (&acc)[2]) {
+#pragma unroll
+  for (int chunk = 0; chunk < 8; ++chunk) {
+    const uint4 v = (chunk & 1)
+                        ? softmax_chunk8<TA_ATTN_POLY_ODD>(&r[chunk * 8], sc2, nm2, weighted, s_w + chunk * 32, acc)
+                        : softmax_chunk8<TA_ATTN_POLY_EVEN>(&r[chunk * 8], sc2, nm2, weighted, s_w + chunk * 32, acc);
+    sts_u4(s_prow + ((chunk ^ (row & 7)) << 4), v);
+  }
+}
+
+__device__ __forceinline__ float f2_total(const uint64_t (&acc)[2]) {
+  const float2 a = f2_unpack(acc[0]), b = f2_unpack(acc[1]);
+  return (a.x + a.y) + (b.x + b.y);
+}
+
+// One warp's 32 query rows x 32 head columns of O / rowsum -> bf16 into a 2 KB smem slab
+// (64-byte rows, SW64 chunk swizzle: conflict-free 16-byte stores), then one TMA store of the
+// slab.  The [B][t][D] output map clips rows >= t, so tail rows need no predication.
+__device__ __forceinline__ void store_o_slab(const CUtensorMap* tmo, const uint32_t* o, float inv,
+                                             uint32_t slab, int lane, int col, int row, int b) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    sts_u4(slab + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4),
+           make_uint4(pack_bf16(__uint_as_float(o[8 * c]) * inv, __uint_as_float(o[8 * c + 1]) * inv),
+                      pack_bf16(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv),
+                      pack_bf16(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv),
+                      pack_bf16(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv)));
+  fence_proxy_async_shared();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_3d_s(tmo, slab, col, row, b);
+    bulk_commit_group();
+  }
+}
+
 template <bool kHasSize>
 __global__ void __launch_bounds__(kThreads, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const float* __restrict__ size, int t,
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo,
+                   const float* __restrict__ size, int t,
                    int H, int n_items, __nv_bfloat16* __restrict__ out, float scale_log2,
                    AttnTcLayout L) {
   extern __shared__ uint8_t smem_raw[];
@@ -297,6 +386,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t s_bias = smem_u32(bias);
     const uint32_t s_red = smem_u32(red);
     const uint32_t s_prow0 = smem_u32(sP) + 2 * g * kPBytes + i * 128;  // + (use & 1) stage
+    // O staging: this warp's 2 KB slab(s) inside its own 32 P rows (4 KB) of the group's first
+    // P stage, which is idle between the tile's last PV MMA (o_full) and the next tile's first
+    // P block; before the warp writes P again the slab's TMA store must have read it
+    // (drain_o_store).  Only the owning warp ever writes these bytes.
+    const uint32_t s_slab = smem_u32(sP) + 2 * g * kPBytes + (warp & 3) * 4096;
+    auto drain_o_store = [&]() {
+      if (lane == 0) bulk_wait_group_read<0>();
+      __syncwarp();
+    };
 
     auto pass1 = [&](uint32_t tcnt) -> float {
       const int ss = tcnt % L.n_s;
@@ -304,7 +402,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&s_full[ss], (tcnt / L.n_s) & 1);
       tc_fence_after();
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#ifdef TA_ATTN_NO_MAX  // profiling only: wrong results
+      m4[0] = 0.f;
+      for (int kb = g; kb < 0; kb += 2) {
+#else
       for (int kb = g; kb < L.n_kb; kb += 2) {
+#endif
         uint32_t r[64];
         tmem_ld_32x32b_x32(la + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
         tmem_ld_32x32b_x32(la + kb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
@@ -331,7 +434,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     auto pass2 = [&](uint32_t tcnt, float mx) -> float {
       const uint32_t la = lane_base + (tcnt % L.n_s) * 256;
-      float s4[4] = {0.f, 0.f, 0.f, 0.f};
+      drain_o_store();
+      uint64_t acc[2] = {0ull, 0ull};
+      const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(-mx, -mx);
       for (int kb = g; kb < L.n_kb; kb += 2, ++use) {
         uint32_t r[64];
         tmem_ld_32x32b_x32(la + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
@@ -343,42 +448,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // p_j = size_j * 2^(s_j * scale - max): the log-size bias as a weight (size 0 masks
         // keys >= t); without a size vector only the last block needs the mask.
         const bool weighted = kHasSize || (kb + 1) * 64 > t;
-        const float nmx = -mx;
-#pragma unroll
-        for (int chunk = 0; chunk < 8; ++chunk) {  // 8 keys = one 16-byte chunk of the P row
-          const uint32_t* rr = &r[chunk * 8];
-          float p0 = ex2_approx(fmaf(__uint_as_float(rr[0]), scale_log2, nmx));
-          float p1 = ex2_approx(fmaf(__uint_as_float(rr[1]), scale_log2, nmx));
-          float p2 = ex2_approx(fmaf(__uint_as_float(rr[2]), scale_log2, nmx));
-          float p3 = ex2_approx(fmaf(__uint_as_float(rr[3]), scale_log2, nmx));
-          float p4 = ex2_approx(fmaf(__uint_as_float(rr[4]), scale_log2, nmx));
-          float p5 = ex2_approx(fmaf(__uint_as_float(rr[5]), scale_log2, nmx));
-          float p6 = ex2_approx(fmaf(__uint_as_float(rr[6]), scale_log2, nmx));
-          float p7 = ex2_approx(fmaf(__uint_as_float(rr[7]), scale_log2, nmx));
-          if (weighted) {
-            const float4 w0 = lds_f4(s_bias + (kb * 64 + chunk * 8) * 4);
-            const float4 w1 = lds_f4(s_bias + (kb * 64 + chunk * 8 + 4) * 4);
-            p0 *= w0.x;
-            p1 *= w0.y;
-            p2 *= w0.z;
-            p3 *= w0.w;
-            p4 *= w1.x;
-            p5 *= w1.y;
-            p6 *= w1.z;
-            p7 *= w1.w;
-          }
-          s4[0] += p0 + p4;
-          s4[1] += p1 + p5;
-          s4[2] += p2 + p6;
-          s4[3] += p3 + p7;
-          sts_u4(s_prow + ((chunk ^ (i & 7)) << 4),
-                 make_uint4(pack_bf16(p0, p1), pack_bf16(p2, p3), pack_bf16(p4, p5), pack_bf16(p6, p7)));
-        }
+        softmax_block64(r, sc2, nm2, weighted, s_bias + kb * 64 * 4, s_prow, i, acc);
         fence_proxy_async_smem();
         tc_fence_before();  // S reads done before the PV MMA may overwrite block 0
         mbar_arrive(&p_full[pst]);
       }
-      sts_f32(s_red + (256 + g * 128 + i) * 4, (s4[0] + s4[1]) + (s4[2] + s4[3]));
+      sts_f32(s_red + (256 + g * 128 + i) * 4, f2_total(acc));
       named_bar_sync(1, 256);
       return rcp_approx(lds_f32(s_red + (256 + i) * 4) + lds_f32(s_red + (384 + i) * 4));
     };
@@ -392,18 +467,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&s_free[ss]);
-      const int q = qt * kQTile + i;
-      if (q < t) {
-        uint4* orow = reinterpret_cast<uint4*>(out + (static_cast<long long>(row_base) + q) * D +
-                                               h * kHd + g * 32);
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          orow[c] = make_uint4(
-              pack_bf16(__uint_as_float(o[8 * c]) * inv, __uint_as_float(o[8 * c + 1]) * inv),
-              pack_bf16(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv),
-              pack_bf16(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv),
-              pack_bf16(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv));
-      }
+      const int q0 = qt * kQTile + (warp & 3) * 32;
+      if (q0 < t) store_o_slab(&tmo, o, inv, s_slab, lane, h * kHd + g * 32, q0, row_base / t);
     };
 
     if (L.rowsplit) {
@@ -452,7 +517,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const float nmx = -fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
           // pass 2: P blocks
-          float s4[4] = {0.f, 0.f, 0.f, 0.f};
+          drain_o_store();
+          uint64_t acc[2] = {0ull, 0ull};
+          const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(nmx, nmx);
           for (int kb = 0; kb < L.n_kb; ++kb, ++use) {
             uint32_t r[64];
             tmem_ld_32x32b_x32(la + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
@@ -462,37 +529,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&p_free[pst], ((use >> 1) & 1) ^ 1);
             tmem_ld_wait();
             const bool weighted = kHasSize || (kb + 1) * 64 > t;
-#pragma unroll
-            for (int chunk = 0; chunk < 8; ++chunk) {
-              const uint32_t* rr = &r[chunk * 8];
-              float p[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e) p[e] = ex2_approx(fmaf(__uint_as_float(rr[e]), scale_log2, nmx));
-              if (weighted) {
-                const float4 w0 = lds_f4(s_bias_g + (kb * 64 + chunk * 8) * 4);
-                const float4 w1 = lds_f4(s_bias_g + (kb * 64 + chunk * 8 + 4) * 4);
-                p[0] *= w0.x;
-                p[1] *= w0.y;
-                p[2] *= w0.z;
-                p[3] *= w0.w;
-                p[4] *= w1.x;
-                p[5] *= w1.y;
-                p[6] *= w1.z;
-                p[7] *= w1.w;
-              }
-              s4[0] += p[0] + p[4];
-              s4[1] += p[1] + p[5];
-              s4[2] += p[2] + p[6];
-              s4[3] += p[3] + p[7];
-              sts_u4(s_prow + ((chunk ^ (i & 7)) << 4),
-                     make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]),
-                                pack_bf16(p[6], p[7])));
-            }
+            softmax_block64(r, sc2, nm2, weighted, s_bias_g + kb * 64 * 4, s_prow, i, acc);
             fence_proxy_async_smem();
             tc_fence_before();  // S reads done before the PV MMA may overwrite block 0
             mbar_arrive(&p_full[pst]);
           }
-          const float inv = rcp_approx((s4[0] + s4[1]) + (s4[2] + s4[3]));
+          const float inv = rcp_approx(f2_total(acc));
           // epilogue: O (64 columns of this slot) / sum -> bf16 row
           mbar_wait(&o_full[g], k & 1);
           tc_fence_after();
@@ -502,18 +544,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_wait();
           tc_fence_before();
           mbar_arrive(&s_free[g]);
-          const int q = qt * kQTile + i;
-          if (q < t) {
-            uint4* orow = reinterpret_cast<uint4*>(out + (static_cast<long long>(row_base) + q) * D + h * kHd);
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              const uint32_t* oo = c < 4 ? &o0[8 * c] : &o1[8 * (c - 4)];
-              orow[c] = make_uint4(
-                  pack_bf16(__uint_as_float(oo[0]) * inv, __uint_as_float(oo[1]) * inv),
-                  pack_bf16(__uint_as_float(oo[2]) * inv, __uint_as_float(oo[3]) * inv),
-                  pack_bf16(__uint_as_float(oo[4]) * inv, __uint_as_float(oo[5]) * inv),
-                  pack_bf16(__uint_as_float(oo[6]) * inv, __uint_as_float(oo[7]) * inv));
-            }
+          const int q0 = qt * kQTile + (warp & 3) * 32;
+          if (q0 < t) {
+            store_o_slab(&tmo, o0, inv, s_slab, lane, h * kHd, q0, b);
+            store_o_slab(&tmo, o1, inv, s_slab + 2048, lane, h * kHd + 32, q0, b);
           }
           ++k;
         }
@@ -573,6 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (pend) epilogue(pend_t, pend_row, pend_h, pend_qt, pend_inv);
     }
+    if (lane == 0) bulk_wait_group<0>();  // O stores complete before the CTA exits
   }
   tc_fence_before();
   __syncthreads();
@@ -592,6 +627,9 @@ int attention_tc(const void* qkv, const float* size, int B, int t, int H, int hd
   const AttnTcLayout L = attn_layout(t);
   CUtensorMap tm;
   int rc = make_tmap_bf16_2d(&tm, qkv, static_cast<uint64_t>(B) * t, 3ull * H * hd, 64);
+  if (rc) return rc;
+  CUtensorMap tmo;
+  rc = make_tmap_attn_out(&tmo, out, B, t, static_cast<uint64_t>(H) * hd);
   if (rc) return rc;
   static bool attr_set = false;
   if (!attr_set) {
@@ -617,8 +655,8 @@ int attention_tc(const void* qkv, const float* size, int B, int t, int H, int hd
   const float scale_log2 = 1.4426950408889634f / 8.0f;
   auto* o = static_cast<__nv_bfloat16*>(out);
   cudaError_t e = size != nullptr
-                      ? cudaLaunchKernelEx(&cfg, attn_tc_kernel<true>, tm, size, t, H, n_items, o, scale_log2, L)
-                      : cudaLaunchKernelEx(&cfg, attn_tc_kernel<false>, tm, size, t, H, n_items, o, scale_log2, L);
+                      ? cudaLaunchKernelEx(&cfg, attn_tc_kernel<true>, tm, tmo, size, t, H, n_items, o, scale_log2, L)
+                      : cudaLaunchKernelEx(&cfg, attn_tc_kernel<false>, tm, tmo, size, t, H, n_items, o, scale_log2, L);
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 

@@ -936,6 +936,22 @@ static int make_tmap_out3(CUtensorMap* map, const void* base, uint64_t images, u
   return r == CUDA_SUCCESS ? TA_OK : TA_ERR_SHAPE;
 }
 
+// Attention output [B][t][D] bf16 as a 3D map with 32-column (64-byte) x 32-row boxes, SW64:
+// one box per softmax warp's O slab (attention_tc.cu store_o_slab); rows >= t are clipped.
+int make_tmap_attn_out(CUtensorMap* map, const void* base, uint64_t images, uint64_t t,
+                       uint64_t cols) {
+  auto enc = get_encode_fn();
+  if (!enc) return TA_ERR_CUDA;
+  cuuint64_t dims[3] = {cols, t, images};
+  cuuint64_t strides[2] = {cols * 2, t * cols * 2};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? TA_OK : TA_ERR_SHAPE;
+}
+
 template <int EPI, typename OutT, bool kRemap = false>
 static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, int N, int K,
                        const GemmEpi& epi, cudaStream_t stream) {

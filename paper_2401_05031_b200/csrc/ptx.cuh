@@ -219,6 +219,14 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
       "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_3d_s(const CUtensorMap* map, uint32_t saddr, int32_t x,
+                                               int32_t y, int32_t z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(saddr), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_commit_group() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -390,6 +398,55 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// ---- packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2: two lanes per issue slot on sm_100)
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2_unpack(uint64_t r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// 2^x for a pair on the FMA pipe instead of the SFU: x = n + f (n = round(x), |f| <= 1/2),
+// 2^f from a degree-3 relative-minimax polynomial (max rel err 7.5e-5, below bf16's 2^-9),
+// 2^n added into the exponent field.  x is clamped to -125 so the result stays a normal
+// (or zero-ish) positive float.  Used for a fraction of the softmax exponentials so the SFU
+// (16 ex2/clk/SM) stops being the attention kernel's bottleneck.
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
+  float2 v = f2_unpack(x);
+  v.x = fmaxf(v.x, -125.f);
+  v.y = fmaxf(v.y, -125.f);
+  const uint64_t xc = f2_pack(v.x, v.y);
+  const uint64_t t = fadd2(xc, f2_pack(12582912.f, 12582912.f));  // 1.5 * 2^23: round to int
+  const uint64_t n = fadd2(t, f2_pack(-12582912.f, -12582912.f));
+  const uint64_t f = ffma2(n, f2_pack(-1.f, -1.f), xc);
+  uint64_t p = ffma2(f2_pack(0.055170562f, 0.055170562f), f, f2_pack(0.24260867f, 0.24260867f));
+  p = ffma2(p, f, f2_pack(0.69326097f, 0.69326097f));
+  p = ffma2(p, f, f2_pack(0.9999283f, 0.9999283f));
+  const float2 pv = f2_unpack(p), tv = f2_unpack(t);
+  // bits(t) = bits(1.5 * 2^23) + n and the low 9 bits of bits(1.5 * 2^23) are zero, so
+  // bits(t) << 23 == n << 23 (mod 2^32)
+  return f2_pack(__uint_as_float(__float_as_uint(pv.x) + (__float_as_uint(tv.x) << 23)),
+                 __uint_as_float(__float_as_uint(pv.y) + (__float_as_uint(tv.y) << 23)));
+}
+
 __device__ __forceinline__ float gelu_erf_fast(float x) {
   // z = |x| / sqrt(2);  exp(-z^2) = 2^(-(|x| * sqrt(log2(e) / 2))^2)
   const float a = fabsf(x);
