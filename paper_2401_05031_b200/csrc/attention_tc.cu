@@ -19,6 +19,7 @@
 // softmax has consumed before the first PV MMA is issued.  Keys past t are masked with a
 // -inf bias (their K / V rows are the next image's rows or TMA zero fill: finite, p = 0).
 #include <cfloat>
+#include <cstdlib>
 
 #include <cudaTypedefs.h>
 
@@ -61,7 +62,11 @@ AttnTcLayout attn_layout(int t) {
   L.n_qt = (t + kQTile - 1) / kQTile;
   L.n_kv = L.t_pad <= 256 ? 2 : 1;
   L.n_s = L.t_pad <= 256 ? 2 : 1;
-  L.rowsplit = L.t_pad <= 128;  // measured: faster for short rows, key split wins at t ~ 197
+  // Row split (each softmax group owns whole tiles of its own S slot) for every t that fits two
+  // slots: measured 121 vs 133 us at t = 197, 51 vs 64 us at t = 101 (B = 256, H = 12).
+  L.rowsplit = L.t_pad <= 256;
+  if (const char* e = getenv("TA_ATTN_SPLIT"))  // profiling override: "row" / "key"
+    L.rowsplit = L.t_pad <= 256 && e[0] != 'k';
   L.kv_bytes = 2u * L.n_kb * kBlkBytes;
   uint32_t off = kQBytes;  // Q: one slot (Q(n+1) is only needed after S(n) has long completed)
   L.kv_off = off;
@@ -77,6 +82,24 @@ AttnTcLayout attn_layout(int t) {
   L.smem_bytes = off + 1024;  // + alignment slack
   return L;
 }
+
+#ifdef TA_ATTN_TRACE  // profiling build only: per-event clock64 timeline of CTA 0
+__device__ unsigned long long g_trace_t[16384];
+__device__ unsigned int g_trace_tag[16384];
+// per-warp slices of 1024 events, register counter: no atomics on the traced path
+#define TRACE(ev)                                                                      \
+  do {                                                                                 \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && tr_n < 1024u) {                  \
+      const unsigned int k_ = (threadIdx.x >> 5) * 1024u + tr_n++;                     \
+      g_trace_t[k_] = clock64();                                                       \
+      g_trace_tag[k_] = (threadIdx.x >> 5) * 256u + (ev);                              \
+    }                                                                                  \
+  } while (0)
+#define TRACE_DECL unsigned int tr_n = 0
+#else
+#define TRACE(ev) do {} while (0)
+#define TRACE_DECL do {} while (0)
+#endif
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -177,6 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const float* __restrict__ size, int t,
                    int H, int n_items, __nv_bfloat16* __restrict__ out, float scale_log2,
                    AttnTcLayout L) {
+  TRACE_DECL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -199,6 +223,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
 
   const uint32_t warp = warp_id(), lane = lane_id();
+  // No runtime integer division in the loops below: it compiles to I2F / MUFU.RCP / F2I on
+  // the SFU, which the softmax exponentials saturate on every sub-partition, and the MMA
+  // issuer then waited ~700 cycles per P block.  Items advance by gridDim.x as (b, h) pairs;
+  // ring indices use n_kv, n_s in {1, 2}.
+  const int step_b = static_cast<int>(gridDim.x) / H;
+  const int step_h = static_cast<int>(gridDim.x) - step_b * H;
+  const int b_first = static_cast<int>(blockIdx.x) / H;
+  const int h_first = static_cast<int>(blockIdx.x) - b_first * H;
+  auto next_bh = [&](int& b, int& h) {
+    b += step_b;
+    h += step_h;
+    if (h >= H) {
+      h -= H;
+      ++b;
+    }
+  };
+  auto ring_slot = [](uint32_t x, int n) -> uint32_t { return n == 2 ? (x & 1u) : 0u; };
+  auto ring_use = [](uint32_t x, int n) -> uint32_t { return n == 2 ? (x >> 1) : x; };
   if (warp == 8 && lane == 0) {
     tma_prefetch(&tm);
     for (int s = 0; s < 2; ++s) {
@@ -230,14 +272,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       uint32_t it = 0, qcnt = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        const int b = item / H, h = item - b * H;
+      int b = b_first, h = h_first;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it, next_bh(b, h)) {
         const int row_base = b * t;
-        const int kvs = it % L.n_kv;
-        const uint32_t kv_use = it / L.n_kv;
+        const int kvs = ring_slot(it, L.n_kv);
+        const uint32_t kv_use = ring_use(it, L.n_kv);
         mbar_wait(&kv_free[kvs], (kv_use & 1) ^ 1);
         uint8_t* sK = sKV + kvs * L.kv_bytes;
         uint8_t* sV = sK + L.n_kb * kBlkBytes;
+        TRACE(1);
         mbar_arrive_expect_tx(&kv_full[kvs], L.kv_bytes);
         for (int kb = 0; kb < L.n_kb; ++kb) {
           tma_load_2d(&tm, &kv_full[kvs], sK + kb * kBlkBytes, D + h * kHd, row_base + kb * kKeyBlk);
@@ -245,9 +288,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int qt = 0; qt < L.n_qt; ++qt, ++qcnt) {
           mbar_wait(&q_free[0], (qcnt & 1) ^ 1);
+#ifdef TA_ATTN_EXP_QONCE  // profiling only: wrong results (Q of the first tile reused)
+          if (qcnt > 0) { mbar_arrive(&q_full[0]); continue; }
+#endif
           mbar_arrive_expect_tx(&q_full[0], kQBytes);
           tma_load_2d(&tm, &q_full[0], sQ, h * kHd, row_base + qt * kQTile);
           tma_load_2d(&tm, &q_full[0], sQ + kBlkBytes, h * kHd, row_base + qt * kQTile + 64);
+          TRACE(2);
         }
       }
     }
@@ -267,6 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t u = p_use[grp]++;
           const int ps = 2 * grp + (u & 1);
           mbar_wait(&p_full[ps], (u >> 1) & 1);
+          TRACE(5);
           tc_fence_after();
           const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
           const uint32_t vbase = smem_u32(sV + kb * kBlkBytes);
@@ -279,24 +327,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma_commit(&p_free[ps]);
         }
         umma_commit(&o_full[sslot]);
+        TRACE(6);
         if (last_of_item) umma_commit(&kv_free[kvs]);
       };
       if (L.rowsplit) {
-        // Row-split mode (t_pad <= 128): tile n lives in S slot n % 2 and is softmaxed by group
+        // Row-split mode (t_pad <= 256): tile n lives in S slot n % 2 and is softmaxed by group
         // n % 2.  Non-blocking scheduler: issue whichever is ready first, the next S (at most two
         // tiles in flight) or the next PV block, so one group never waits on the other.
         const int n_my = n_items > static_cast<int>(blockIdx.x)
                              ? (n_items - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
                              : 0;
         const int T = n_my * L.n_qt;
-        int sN = 0, pN = 0, pkb = 0;
-        while (pN < T) {
-          if (sN < T && sN < pN + 2) {
-            const int it = sN / L.n_qt, qt = sN - it * L.n_qt;
+        // Tile n uses S slot n % 2 and softmax group n % 2; each group's PV blocks are issued
+        // as soon as they are ready, independently of the other group (the O accumulators are
+        // per slot), so the two groups overlap instead of taking turns.
+        int sN = 0, pdone = 0;
+        int s_it = 0, s_qt = 0;  // (item, q tile) of tile sN
+        int pt[2] = {0, 1}, pkb[2] = {0, 0};
+        // (item, q tile) of each group's current PV tile pt[g]
+        int p_it[2] = {0, L.n_qt == 1 ? 1 : 0}, p_qt[2] = {0, L.n_qt == 1 ? 0 : 1};
+        int kv_tiles[2] = {0, 0};  // per K/V slot: tiles of the slot's item whose PV is issued
+        while (pdone < T) {
+          if (sN < T) {
             const int slot = sN & 1;
-            const int kvs = it % L.n_kv;
+            const int kvs = ring_slot(s_it, L.n_kv);
             if (mbar_test(&s_free[slot], ((sN >> 1) & 1) ^ 1) && mbar_test(&q_full[0], sN & 1) &&
-                (qt != 0 || mbar_test(&kv_full[kvs], (it / L.n_kv) & 1))) {
+                (s_qt != 0 || mbar_test(&kv_full[kvs], ring_use(s_it, L.n_kv) & 1))) {
+              TRACE(7);
               tc_fence_after();
               const uint8_t* sK = sKV + kvs * L.kv_bytes;
               const uint64_t qdesc = umma_desc_sw128(smem_u32(sQ));
@@ -307,51 +364,68 @@ __global__ void __launch_bounds__(kThreads, 1)
                 umma_f16(tmem + slot * 256, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0);
               umma_commit(&s_full[slot]);
               umma_commit(&q_free[0]);
+              TRACE(4);
               ++sN;
+              if (++s_qt == L.n_qt) {
+                s_qt = 0;
+                ++s_it;
+              }
             }
           }
-          if (pN < sN) {
-            const int grp = pN & 1;
+#pragma unroll
+          for (int grp = 0; grp < 2; ++grp) {
+            if (pt[grp] >= sN) continue;
             const uint32_t u = p_use[grp];
             const int ps = 2 * grp + (u & 1);
-            if (mbar_test(&p_full[ps], (u >> 1) & 1)) {
-              ++p_use[grp];
-              tc_fence_after();
-              const int it = pN / L.n_qt, qt = pN - it * L.n_qt;
-              const int kvs = it % L.n_kv;
-              const uint8_t* sV = sKV + kvs * L.kv_bytes + L.n_kb * kBlkBytes;
-              const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
-              const uint32_t vbase = smem_u32(sV + pkb * kBlkBytes);
+            if (!mbar_test(&p_full[ps], (u >> 1) & 1)) continue;
+            TRACE(8 + 16 * grp);
+            ++p_use[grp];
+            tc_fence_after();
+            const int kvs = ring_slot(p_it[grp], L.n_kv);
+            const uint8_t* sV = sKV + kvs * L.kv_bytes + L.n_kb * kBlkBytes;
+            const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
+            const uint32_t vbase = smem_u32(sV + pkb[grp] * kBlkBytes);
 #pragma unroll
-              for (int kc = 0; kc < kKeyBlk / 16; ++kc) {
-                const uint64_t vdesc = umma_desc_sw128_mn(vbase + kc * 2048, 8192, 1024);
-                umma_f16(tmem + grp * 256, pdesc + 2 * kc, vdesc, idesc_pv, (pkb | kc) != 0);
+            for (int kc = 0; kc < kKeyBlk / 16; ++kc) {
+              const uint64_t vdesc = umma_desc_sw128_mn(vbase + kc * 2048, 8192, 1024);
+              umma_f16(tmem + grp * 256, pdesc + 2 * kc, vdesc, idesc_pv, (pkb[grp] | kc) != 0);
+            }
+            umma_commit(&p_free[ps]);
+            TRACE(5 + 16 * grp);
+            if (++pkb[grp] == L.n_kb) {
+              umma_commit(&o_full[grp]);
+              TRACE(6);
+              if (++kv_tiles[kvs] == L.n_qt) {  // every tile of the item has its PV issued
+                umma_commit(&kv_free[kvs]);
+                kv_tiles[kvs] = 0;
               }
-              umma_commit(&p_free[ps]);
-              if (++pkb == L.n_kb) {
-                umma_commit(&o_full[grp]);
-                if (qt + 1 == L.n_qt) umma_commit(&kv_free[kvs]);
-                ++pN;
-                pkb = 0;
+              pt[grp] += 2;
+              p_qt[grp] += 2;
+              while (p_qt[grp] >= L.n_qt) {
+                p_qt[grp] -= L.n_qt;
+                ++p_it[grp];
               }
+              pkb[grp] = 0;
+              ++pdone;
             }
           }
         }
       } else {
       uint32_t it = 0, qcnt = 0, tcnt = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        const int kvs = it % L.n_kv;
-        const uint32_t kv_use = it / L.n_kv;
+        const int kvs = ring_slot(it, L.n_kv);
+        const uint32_t kv_use = ring_use(it, L.n_kv);
         const uint8_t* sK = sKV + kvs * L.kv_bytes;
         for (int qt = 0; qt < L.n_qt; ++qt, ++qcnt, ++tcnt) {
-          const int ss = tcnt % L.n_s;
+          const int ss = ring_slot(tcnt, L.n_s);
           if (L.n_s == 1 && pend_slot >= 0) {  // single S slot: finish the previous tile first
             issue_pv(pend_slot, pend_kvs, pend_last);
             pend_slot = -1;
           }
-          mbar_wait(&s_free[ss], ((tcnt / L.n_s) & 1) ^ 1);
+          mbar_wait(&s_free[ss], (ring_use(tcnt, L.n_s) & 1) ^ 1);
           mbar_wait(&q_full[0], qcnt & 1);
           if (qt == 0) mbar_wait(&kv_full[kvs], kv_use & 1);
+          TRACE(3);
           tc_fence_after();
           const uint64_t qdesc = umma_desc_sw128(smem_u32(sQ));
           for (int n0 = 0; n0 < L.t_pad; n0 += 256) {
@@ -363,6 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               umma_f16(tmem + ss * 256 + n0, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0);
           }
           umma_commit(&s_full[ss]);
+          TRACE(4);
           umma_commit(&q_free[0]);
           if (pend_slot >= 0) issue_pv(pend_slot, pend_kvs, pend_last);
           pend_slot = ss;
@@ -397,9 +472,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
 
     auto pass1 = [&](uint32_t tcnt) -> float {
-      const int ss = tcnt % L.n_s;
+      const int ss = ring_slot(tcnt, L.n_s);
       const uint32_t la = lane_base + ss * 256;
-      mbar_wait(&s_full[ss], (tcnt / L.n_s) & 1);
+      mbar_wait(&s_full[ss], ring_use(tcnt, L.n_s) & 1);
+      TRACE(10);
       tc_fence_after();
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #ifdef TA_ATTN_NO_MAX  // profiling only: wrong results
@@ -427,13 +503,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       sts_f32(s_red + (g * 128 + i) * 4, fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])));
+      TRACE(11);
       named_bar_sync(1, 256);
+      TRACE(12);
       // row max of the raw scores, in the scaled log2 domain
       return fmaxf(lds_f32(s_red + i * 4), lds_f32(s_red + (128 + i) * 4)) * scale_log2;
     };
 
     auto pass2 = [&](uint32_t tcnt, float mx) -> float {
-      const uint32_t la = lane_base + (tcnt % L.n_s) * 256;
+      const uint32_t la = lane_base + ring_slot(tcnt, L.n_s) * 256;
       drain_o_store();
       uint64_t acc[2] = {0ull, 0ull};
       const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(-mx, -mx);
@@ -444,6 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int pst = 2 * g + (use & 1);
         const uint32_t s_prow = s_prow0 + (use & 1) * kPBytes;
         mbar_wait(&p_free[pst], ((use >> 1) & 1) ^ 1);
+        TRACE(13);
         tmem_ld_wait();
         // p_j = size_j * 2^(s_j * scale - max): the log-size bias as a weight (size 0 masks
         // keys >= t); without a size vector only the last block needs the mask.
@@ -452,15 +531,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         tc_fence_before();  // S reads done before the PV MMA may overwrite block 0
         mbar_arrive(&p_full[pst]);
+        TRACE(14);
       }
+      TRACE(15);
       sts_f32(s_red + (256 + g * 128 + i) * 4, f2_total(acc));
       named_bar_sync(1, 256);
+      TRACE(16);
       return rcp_approx(lds_f32(s_red + (256 + i) * 4) + lds_f32(s_red + (384 + i) * 4));
     };
 
-    auto epilogue = [&](uint32_t tcnt, int row_base, int h, int qt, float inv) {
-      const int ss = tcnt % L.n_s;
-      mbar_wait(&o_full[ss], (tcnt / L.n_s) & 1);
+    auto epilogue = [&](uint32_t tcnt, int b, int h, int qt, float inv) {
+      const int ss = ring_slot(tcnt, L.n_s);
+      mbar_wait(&o_full[ss], ring_use(tcnt, L.n_s) & 1);
+      TRACE(17);
       tc_fence_after();
       uint32_t o[32];
       tmem_ld_32x32b_x32(lane_base + ss * 256 + g * 32, o);
@@ -468,7 +551,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&s_free[ss]);
       const int q0 = qt * kQTile + (warp & 3) * 32;
-      if (q0 < t) store_o_slab(&tmo, o, inv, s_slab, lane, h * kHd + g * 32, q0, row_base / t);
+      if (q0 < t) store_o_slab(&tmo, o, inv, s_slab, lane, h * kHd + g * 32, q0, b);
+      TRACE(18);
     };
 
     if (L.rowsplit) {
@@ -478,8 +562,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t la = lane_base + g * 256;
       uint32_t k = 0;  // tiles processed by this group
       uint32_t tile = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const int b = item / H, h = item - b * H;
+      int b = b_first, h = h_first;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, next_bh(b, h)) {
         const int row_base = b * t;
         bool have_bias = false;
         for (int qt = 0; qt < L.n_qt; ++qt, ++tile) {
@@ -493,6 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             have_bias = true;
           }
           mbar_wait(&s_full[g], k & 1);
+          TRACE(10);
           tc_fence_after();
           // pass 1: row max of the raw scores over the valid keys
           float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
@@ -515,6 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (kb * 64 + j < t) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(r[j]));
             }
           }
+          TRACE(11);
           const float nmx = -fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
           // pass 2: P blocks
           drain_o_store();
@@ -527,16 +613,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int pst = 2 * g + (use & 1);
             const uint32_t s_prow = s_prow0 + (use & 1) * kPBytes;
             mbar_wait(&p_free[pst], ((use >> 1) & 1) ^ 1);
+            TRACE(13);
             tmem_ld_wait();
             const bool weighted = kHasSize || (kb + 1) * 64 > t;
             softmax_block64(r, sc2, nm2, weighted, s_bias_g + kb * 64 * 4, s_prow, i, acc);
             fence_proxy_async_smem();
             tc_fence_before();  // S reads done before the PV MMA may overwrite block 0
             mbar_arrive(&p_full[pst]);
+            TRACE(14);
           }
           const float inv = rcp_approx(f2_total(acc));
           // epilogue: O (64 columns of this slot) / sum -> bf16 row
           mbar_wait(&o_full[g], k & 1);
+          TRACE(17);
           tc_fence_after();
           uint32_t o0[32], o1[32];
           tmem_ld_32x32b_x32(la, o0);
@@ -549,6 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             store_o_slab(&tmo, o0, inv, s_slab, lane, h * kHd, q0, b);
             store_o_slab(&tmo, o1, inv, s_slab + 2048, lane, h * kHd + 32, q0, b);
           }
+          TRACE(18);
           ++k;
         }
       }
@@ -560,8 +650,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     float pend_inv = 0.f;
     uint32_t tcnt = 0;
     // log2(size) of the item's keys j = threadIdx.x + 256 k (k < 2), loaded one item ahead
-    auto load_bias = [&](int item, float (&v)[2]) {
-      const int row_base_n = (item / H) * t;
+    auto load_bias = [&](int b_n, float (&v)[2]) {
+      const int row_base_n = b_n * t;
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         const int j = threadIdx.x + 256 * k;
@@ -569,12 +659,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     float sz_next[2];
-    if (blockIdx.x < n_items) load_bias(blockIdx.x, sz_next);
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int b = item / H, h = item - b * H;
-      const int row_base = b * t;
+    if (static_cast<int>(blockIdx.x) < n_items) load_bias(b_first, sz_next);
+    int b = b_first, h = h_first;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, next_bh(b, h)) {
       float sz[2] = {sz_next[0], sz_next[1]};
-      if (item + static_cast<int>(gridDim.x) < n_items) load_bias(item + gridDim.x, sz_next);
+      if (item + static_cast<int>(gridDim.x) < n_items) {
+        int bn = b, hn = h;
+        next_bh(bn, hn);
+        load_bias(bn, sz_next);
+      }
       if (pend) {  // bias is rewritten below; the deferred epilogue does not read it
         epilogue(pend_t, pend_row, pend_h, pend_qt, pend_inv);
         pend = false;
@@ -596,12 +689,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (L.n_s == 2) {
           pend = true;
           pend_t = tcnt;
-          pend_row = row_base;
+          pend_row = b;
           pend_h = h;
           pend_qt = qt;
           pend_inv = inv;
         } else {
-          epilogue(tcnt, row_base, h, qt, inv);
+          epilogue(tcnt, b, h, qt, inv);
         }
       }
     }
@@ -660,4 +753,18 @@ int attention_tc(const void* qkv, const float* size, int B, int t, int H, int hd
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 
+#ifdef TA_ATTN_TRACE
+extern "C" __attribute__((visibility("default"))) int ta_debug_attn_trace(unsigned long long* t,
+                                                                        unsigned int* tag, int max,
+                                                                        int reset) {
+  // tag 0 = empty slot (event ids start at 1)
+  static unsigned int zeros[16384];
+  if (reset) return cudaMemcpyToSymbol(g_trace_tag, zeros, sizeof(zeros)) == cudaSuccess ? 0 : -1;
+  cudaDeviceSynchronize();
+  const int n = max < 16384 ? max : 16384;
+  cudaMemcpyFromSymbol(t, g_trace_t, n * sizeof(unsigned long long));
+  cudaMemcpyFromSymbol(tag, g_trace_tag, n * sizeof(unsigned int));
+  return n;
+}
+#endif
 }  // namespace ta

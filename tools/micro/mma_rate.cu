@@ -1,0 +1,112 @@
+// tcgen05.mma issue-to-completion rate for the attention shapes, one CTA per SM, one issuing
+// thread: S = Q K^T (M=128, N=256, K-major both) and PV (M=128, N=64, B MN-major) on zeroed
+// smem.  Prints clk per MMA instruction (floor: 128*N/256).
+#include <cstdio>
+#include "../../paper_2401_05031_b200/csrc/ptx.cuh"
+using namespace ta;
+
+template <int kMode, int kLoad>  // 0: S shape, 1: PV shape (MN-major B), 2: PV shape, K-major B
+__global__ void mma_rate(unsigned long long* out, int iters) {
+  __shared__ volatile int done;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t slot;
+  __shared__ uint64_t bar, bar2;
+  for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x3c003c01u * (i + 1), 0xbc013c02u ^ (i * 2654435761u), 0x3e00bc00u + i, 0x3c00c000u ^ (i * 40503u));
+  if (threadIdx.x < 32) tmem_alloc<512>(&slot);
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&bar2, 1); fence_barrier_init(); done = 0; }
+  fence_proxy_async_shared();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    const uint32_t tmem = slot;
+    const uint64_t a = umma_desc_sw128(smem_u32(smem));
+    const uint64_t b = umma_desc_sw128(smem_u32(smem + 32768));
+    const uint32_t id_s = idesc_bf16(128, 256);
+    const uint32_t id_pv = idesc_bf16(128, 64, true);
+    const uint32_t id_pvk = idesc_bf16(128, 64, false);
+    const uint32_t vbase = smem_u32(smem + 32768);
+    const unsigned long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      if (kMode == 3) {  // kernel pattern: S + commit, then 4 PV blocks each + commit
+#pragma unroll
+        for (int k = 0; k < 4; ++k) umma_f16(tmem + 256, a + 2 * k, b + 2 * k, id_s, k > 0);
+        umma_commit(&bar2);
+        for (int kb = 0; kb < 4; ++kb) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_f16(tmem, a + 2 * k, umma_desc_sw128_mn(vbase + kb * 8192 + k * 2048, 8192, 1024), id_pv, (kb | k) != 0);
+          umma_commit(&bar2);
+        }
+        continue;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (kMode == 0) umma_f16(tmem, a + 2 * k, b + 2 * k, id_s, 1);
+        else if (kMode == 1) umma_f16(tmem, a + 2 * k, umma_desc_sw128_mn(vbase + k * 2048, 8192, 1024), id_pv, 1);
+        else umma_f16(tmem, a + 2 * k, b + 2 * k, id_pvk, 1);
+      }
+    }
+    umma_commit(&bar);
+    mbar_wait(&bar, 0);
+    const unsigned long long t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+    done = 1;
+  }
+  if (kLoad == 2 && threadIdx.x >= 128) {  // 8 warps storing 16 B chunks into smem 64..96 KB
+    uint32_t addr = smem_u32(smem + 65536) + (threadIdx.x - 128) * 16;
+    uint32_t k = 0;
+    while (!done) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sts_u4(addr + ((k + j) & 7) * 4096, make_uint4(k, j, k, j));
+      ++k;
+    }
+  }
+  if ((kLoad == 1 || kLoad == 3) && threadIdx.x >= 128) {  // 8 warps streaming TMEM loads
+    // kLoad 1: columns 256..511 (other half); 3: columns 64..319 (same half as the PV output)
+    const uint32_t base = slot + ((((threadIdx.x >> 5) & 3) * 32u) << 16) + (kLoad == 1 ? 256 : 64);
+    float acc = 0.f;
+    while (!done) {
+      for (int c = 0; c < 256; c += 64) {
+        uint32_t r[32], q[32];
+        tmem_ld_32x32b_x32(base + c, r);
+        tmem_ld_32x32b_x32(base + c + 32, q);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc = fmaxf(acc, fmaxf(__uint_as_float(r[j]), __uint_as_float(q[j])));
+      }
+    }
+    if (acc == 1234.f) out[0] = 0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) { tc_fence_after(); tmem_dealloc<512>(slot); }
+}
+
+template <int M, int L>
+void run(const char* name, unsigned long long* d, double floor) {
+  const int iters = 2000;
+  cudaFuncSetAttribute(mma_rate<M, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  for (int rep = 0; rep < 2; ++rep) mma_rate<M, L><<<148, L ? 384 : 128, 100 * 1024>>>(d, iters);
+  cudaDeviceSynchronize();
+  unsigned long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < 148; ++i) avg += h[i];
+  avg /= 148;
+  printf("%-28s %7.1f clk/MMA (floor %.0f)  %s\n", name, avg / (iters * 4.0), floor,
+         cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  unsigned long long* d;
+  cudaMalloc(&d, 148 * sizeof(unsigned long long));
+  run<1, 0>("PV  M128 N64", d, 32);
+  run<1, 1>("PV  + ld cols 256..511", d, 32);
+  run<1, 3>("PV  + ld cols 64..319", d, 32);
+  run<3, 1>("pattern /4 + ld other half", d, 0);
+  run<3, 3>("pattern /4 + ld cols 64..319", d, 0);
+  return 0;
+}
