@@ -235,7 +235,10 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     value = imgs_total / (total_ms / 1e3)
-    peak, peak_sus, hbm, peak_src = _peaks()
+    peak_burst, peak_sus, hbm, peak_src = _peaks()
+    # the forward is timed inside a long step (tens of ms of back-to-back tensor work), so the
+    # roofline denominator is the SUSTAINED bf16 figure; the burst one is reported beside it
+    peak = peak_sus or peak_burst
     flops = {g: flops_per_image(cfg, g) for g in gammas}
     sweep_flops = sum(flops[g] * B for g in gammas) * args.steps
     achieved = sweep_flops / (total_ms / 1e3) / 1e12  # per GPU
@@ -245,10 +248,10 @@ def run_ours(args):
         tf = ips * flops[g] / 1e12
         per_gamma[str(g)] = {"images_per_s": round(ips, 1), "ms_per_batch": round(per_gamma_ms[g] / args.steps, 3),
                              "gflop_per_image": round(flops[g] / 1e9, 3), "tflops": round(tf, 1),
-                             "roofline_frac": round(tf / peak, 4)}
+                             "roofline_frac": round(tf / peak, 4), "frac_of_burst": round(tf / peak_burst, 4)}
 
     # dominant kernel alone: fc1 GEMM at the gamma=0 shape (M = B*197, N = 4D, K = D)
-    dom = dominant_gemm(cfg, B, dev, peak)
+    dom = dominant_gemm(cfg, B, dev, peak_burst)  # timed alone: burst peak
 
     # e2e through the public API: pinned host images -> ServeModel.forward -> host logits
     e2e_ips, h2d, d2h = run_e2e(sm, cfg, B, gammas, args, dev)
@@ -278,8 +281,8 @@ def run_ours(args):
             "per_gamma": per_gamma,
             "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
                          "frac": round(achieved / peak, 4), "traffic": None,
-                         "peak_source": f"{peak_src} bf16_tflops (burst); sustained {peak_sus}",
-                         "frac_of_sustained": round(achieved / peak_sus, 4) if peak_sus else None,
+                         "peak_source": f"{peak_src} bf16_tflops_sustained (burst {peak_burst})",
+                         "frac_of_burst": round(achieved / peak_burst, 4),
                          "what": "whole forward: algorithmic FLOPs (SURVEY.md §8d F(model, gamma) x images) / device time"},
             "dominant_kernel": dom,
             "e2e": {"value": round(e2e_ips, 1), "unit": "images/s", "h2d_bytes_per_step": h2d,

@@ -46,6 +46,9 @@ constexpr int kThreads = 320;
 
 struct AttnTcLayout {
   int t_pad;    // round_up(t, 64)
+  int t_mma;    // round_up(t, 16): S MMA N (keys past it are never read)
+  int nch_last; // 8-key chunks of the last 64-key block holding keys < t
+  int nkc_last; // 16-key PV steps of the last block (chunks [nch_last, 2 nkc_last) are zeros)
   int n_kb;     // t_pad / 64
   int n_qt;     // ceil(t / 128)
   int n_kv;     // K/V ring slots (2 when t_pad <= 256)
@@ -59,6 +62,12 @@ AttnTcLayout attn_layout(int t) {
   AttnTcLayout L{};
   L.t_pad = (t + kKeyBlk - 1) / kKeyBlk * kKeyBlk;
   L.n_kb = L.t_pad / kKeyBlk;
+  L.t_mma = (t + 15) / 16 * 16;
+  {
+    const int rem = t - (L.n_kb - 1) * kKeyBlk;  // 1..64 keys in the last block
+    L.nch_last = (rem + 7) / 8;
+    L.nkc_last = (rem + 15) / 16;
+  }
   L.n_qt = (t + kQTile - 1) / kQTile;
   L.n_kv = L.t_pad <= 256 ? 2 : 1;
   L.n_s = L.t_pad <= 256 ? 2 : 1;
@@ -166,6 +175,44 @@ __device__ __forceinline__ void softmax_block64(const uint32_t (&r)[64], uint64_
                         ? softmax_chunk8<TA_ATTN_POLY_ODD>(&r[chunk * 8], sc2, nm2, weighted, s_w + chunk * 32, acc)
                         : softmax_chunk8<TA_ATTN_POLY_EVEN>(&r[chunk * 8], sc2, nm2, weighted, s_w + chunk * 32, acc);
     sts_u4(s_prow + ((chunk ^ (row & 7)) << 4), v);
+  }
+}
+
+// Last 64-key block: only its first nch chunks hold keys < t (8 nch <= t_mma - 64 kb); the
+// chunks up to the PV MMA's K extent (2 nkc) are written as zeros, the rest are never read.
+__device__ __forceinline__ void softmax_block_tail(const uint32_t (&r)[64], uint64_t sc2, uint64_t nm2,
+                                                   uint32_t s_w, uint32_t s_prow, int row, int nch,
+                                                   int nzero, uint64_t (&acc)[2]) {
+#pragma unroll
+  for (int chunk = 0; chunk < 8; ++chunk) {
+    if (chunk >= nzero) break;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (chunk < nch)
+      v = (chunk & 1) ? softmax_chunk8<TA_ATTN_POLY_ODD>(&r[chunk * 8], sc2, nm2, true, s_w + chunk * 32, acc)
+                      : softmax_chunk8<TA_ATTN_POLY_EVEN>(&r[chunk * 8], sc2, nm2, true, s_w + chunk * 32, acc);
+    sts_u4(s_prow + ((chunk ^ (row & 7)) << 4), v);
+  }
+}
+
+// Row max of the raw scores of one 64-key block over its first `valid` keys (the second
+// 32-column half is not loaded when it holds no valid key).
+__device__ __forceinline__ void block_max(uint32_t ta, int valid, float (&m4)[4]) {
+  uint32_t r[64];
+  tmem_ld_32x32b_x32(ta, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+  tmem_ld_32x32b_x32(ta + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+  tmem_ld_wait();
+  if (valid == 64) {
+#pragma unroll
+    for (int j = 0; j < 64; j += 4) {
+      m4[0] = fmaxf(m4[0], __uint_as_float(r[j]));
+      m4[1] = fmaxf(m4[1], __uint_as_float(r[j + 1]));
+      m4[2] = fmaxf(m4[2], __uint_as_float(r[j + 2]));
+      m4[3] = fmaxf(m4[3], __uint_as_float(r[j + 3]));
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 64; ++j)
+      if (j < valid) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(r[j]));
   }
 }
 
@@ -318,8 +365,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
           const uint32_t vbase = smem_u32(sV + kb * kBlkBytes);
+          const int nkc = kb == L.n_kb - 1 ? L.nkc_last : kKeyBlk / 16;
 #pragma unroll
           for (int kc = 0; kc < kKeyBlk / 16; ++kc) {
+            if (kc >= nkc) break;
             // V rows (keys) are the K dimension: 16 keys = two 8-row groups = 2048 B.
             const uint64_t vdesc = umma_desc_sw128_mn(vbase + kc * 2048, 8192, 1024);
             umma_f16(o_tmem, pdesc + 2 * kc, vdesc, idesc_pv, (kb | kc) != 0);
@@ -357,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tc_fence_after();
               const uint8_t* sK = sKV + kvs * L.kv_bytes;
               const uint64_t qdesc = umma_desc_sw128(smem_u32(sQ));
-              const uint32_t idesc_s = idesc_bf16(kQTile, L.t_pad);
+              const uint32_t idesc_s = idesc_bf16(kQTile, L.t_mma);
               const uint64_t kdesc = umma_desc_sw128(smem_u32(sK));
 #pragma unroll
               for (int k = 0; k < kHd / 16; ++k)
@@ -385,8 +434,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint8_t* sV = sKV + kvs * L.kv_bytes + L.n_kb * kBlkBytes;
             const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
             const uint32_t vbase = smem_u32(sV + pkb[grp] * kBlkBytes);
+            const int nkc = pkb[grp] == L.n_kb - 1 ? L.nkc_last : kKeyBlk / 16;
 #pragma unroll
             for (int kc = 0; kc < kKeyBlk / 16; ++kc) {
+              if (kc >= nkc) break;
               const uint64_t vdesc = umma_desc_sw128_mn(vbase + kc * 2048, 8192, 1024);
               umma_f16(tmem + grp * 256, pdesc + 2 * kc, vdesc, idesc_pv, (pkb[grp] | kc) != 0);
             }
@@ -428,8 +479,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           TRACE(3);
           tc_fence_after();
           const uint64_t qdesc = umma_desc_sw128(smem_u32(sQ));
-          for (int n0 = 0; n0 < L.t_pad; n0 += 256) {
-            const int n = L.t_pad - n0 < 256 ? L.t_pad - n0 : 256;
+          for (int n0 = 0; n0 < L.t_mma; n0 += 256) {
+            const int n = L.t_mma - n0 < 256 ? L.t_mma - n0 : 256;
             const uint32_t idesc_s = idesc_bf16(kQTile, n);
             const uint64_t kdesc = umma_desc_sw128(smem_u32(sK + n0 * 128));
 #pragma unroll
@@ -471,37 +522,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
     };
 
-    auto pass1 = [&](uint32_t tcnt) -> float {
+    // a warp whose 32 query rows of tile qt all lie past t only keeps the barrier protocol
+    auto row_idle = [&](int qt) { return qt * kQTile + static_cast<int>(warp & 3) * 32 >= t; };
+    auto pass1 = [&](uint32_t tcnt, int qt) -> float {
       const int ss = ring_slot(tcnt, L.n_s);
       const uint32_t la = lane_base + ss * 256;
       mbar_wait(&s_full[ss], ring_use(tcnt, L.n_s) & 1);
       TRACE(10);
       tc_fence_after();
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#ifdef TA_ATTN_NO_MAX  // profiling only: wrong results
-      m4[0] = 0.f;
-      for (int kb = g; kb < 0; kb += 2) {
-#else
-      for (int kb = g; kb < L.n_kb; kb += 2) {
-#endif
-        uint32_t r[64];
-        tmem_ld_32x32b_x32(la + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-        tmem_ld_32x32b_x32(la + kb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-        tmem_ld_wait();
-        if ((kb + 1) * 64 <= t) {
-#pragma unroll
-          for (int j = 0; j < 64; j += 4) {
-            m4[0] = fmaxf(m4[0], __uint_as_float(r[j]));
-            m4[1] = fmaxf(m4[1], __uint_as_float(r[j + 1]));
-            m4[2] = fmaxf(m4[2], __uint_as_float(r[j + 2]));
-            m4[3] = fmaxf(m4[3], __uint_as_float(r[j + 3]));
-          }
-        } else {  // last block: keys >= t are not part of the row
-#pragma unroll
-          for (int j = 0; j < 64; ++j)
-            if (kb * 64 + j < t) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(r[j]));
-        }
-      }
+      if (!row_idle(qt))
+        for (int kb = g; kb < L.n_kb; kb += 2) block_max(la + kb * 64, min(kKeyBlk, t - kb * kKeyBlk), m4);
       sts_f32(s_red + (g * 128 + i) * 4, fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])));
       TRACE(11);
       named_bar_sync(1, 256);
@@ -510,25 +541,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       return fmaxf(lds_f32(s_red + i * 4), lds_f32(s_red + (128 + i) * 4)) * scale_log2;
     };
 
-    auto pass2 = [&](uint32_t tcnt, float mx) -> float {
+    auto pass2 = [&](uint32_t tcnt, float mx, int qt) -> float {
       const uint32_t la = lane_base + ring_slot(tcnt, L.n_s) * 256;
+      const bool idle = row_idle(qt);
       drain_o_store();
       uint64_t acc[2] = {0ull, 0ull};
       const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(-mx, -mx);
       for (int kb = g; kb < L.n_kb; kb += 2, ++use) {
+        const bool last = kb == L.n_kb - 1;
         uint32_t r[64];
-        tmem_ld_32x32b_x32(la + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-        tmem_ld_32x32b_x32(la + kb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+        if (!idle) {
+          tmem_ld_32x32b_x32(la + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          tmem_ld_32x32b_x32(la + kb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+        }
         const int pst = 2 * g + (use & 1);
         const uint32_t s_prow = s_prow0 + (use & 1) * kPBytes;
         mbar_wait(&p_free[pst], ((use >> 1) & 1) ^ 1);
         TRACE(13);
-        tmem_ld_wait();
-        // p_j = size_j * 2^(s_j * scale - max): the log-size bias as a weight (size 0 masks
-        // keys >= t); without a size vector only the last block needs the mask.
-        const bool weighted = kHasSize || (kb + 1) * 64 > t;
-        softmax_block64(r, sc2, nm2, weighted, s_bias + kb * 64 * 4, s_prow, i, acc);
-        fence_proxy_async_smem();
+        if (!idle) {
+          tmem_ld_wait();
+          // p_j = size_j * 2^(s_j * scale - max): the log-size bias as a weight (size 0 masks
+          // keys >= t); without a size vector only the last block needs the mask.
+          if (!last)
+            softmax_block64(r, sc2, nm2, kHasSize, s_bias + kb * 64 * 4, s_prow, i, acc);
+          else
+            softmax_block_tail(r, sc2, nm2, s_bias + kb * 64 * 4, s_prow, i, L.nch_last,
+                               2 * L.nkc_last, acc);
+          fence_proxy_async_smem();
+        }
         tc_fence_before();  // S reads done before the PV MMA may overwrite block 0
         mbar_arrive(&p_full[pst]);
         TRACE(14);
@@ -579,27 +619,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&s_full[g], k & 1);
           TRACE(10);
           tc_fence_after();
+          const bool idle = row_idle(qt);
           // pass 1: row max of the raw scores over the valid keys
           float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-          for (int kb = 0; kb < L.n_kb; ++kb) {
-            uint32_t r[64];
-            tmem_ld_32x32b_x32(la + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-            tmem_ld_32x32b_x32(la + kb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-            tmem_ld_wait();
-            if ((kb + 1) * 64 <= t) {
-#pragma unroll
-              for (int j = 0; j < 64; j += 4) {
-                m4[0] = fmaxf(m4[0], __uint_as_float(r[j]));
-                m4[1] = fmaxf(m4[1], __uint_as_float(r[j + 1]));
-                m4[2] = fmaxf(m4[2], __uint_as_float(r[j + 2]));
-                m4[3] = fmaxf(m4[3], __uint_as_float(r[j + 3]));
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 64; ++j)
-                if (kb * 64 + j < t) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(r[j]));
-            }
-          }
+          if (!idle)
+            for (int kb = 0; kb < L.n_kb; ++kb) block_max(la + kb * 64, min(kKeyBlk, t - kb * kKeyBlk), m4);
           TRACE(11);
           const float nmx = -fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
           // pass 2: P blocks
@@ -607,17 +631,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint64_t acc[2] = {0ull, 0ull};
           const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(nmx, nmx);
           for (int kb = 0; kb < L.n_kb; ++kb, ++use) {
+            const bool last = kb == L.n_kb - 1;
             uint32_t r[64];
-            tmem_ld_32x32b_x32(la + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-            tmem_ld_32x32b_x32(la + kb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+            if (!idle) {
+              tmem_ld_32x32b_x32(la + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+              tmem_ld_32x32b_x32(la + kb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+            }
             const int pst = 2 * g + (use & 1);
             const uint32_t s_prow = s_prow0 + (use & 1) * kPBytes;
             mbar_wait(&p_free[pst], ((use >> 1) & 1) ^ 1);
             TRACE(13);
-            tmem_ld_wait();
-            const bool weighted = kHasSize || (kb + 1) * 64 > t;
-            softmax_block64(r, sc2, nm2, weighted, s_bias_g + kb * 64 * 4, s_prow, i, acc);
-            fence_proxy_async_smem();
+            if (!idle) {
+              tmem_ld_wait();
+              if (!last)
+                softmax_block64(r, sc2, nm2, kHasSize, s_bias_g + kb * 64 * 4, s_prow, i, acc);
+              else
+                softmax_block_tail(r, sc2, nm2, s_bias_g + kb * 64 * 4, s_prow, i, L.nch_last,
+                                   2 * L.nkc_last, acc);
+              fence_proxy_async_smem();
+            }
             tc_fence_before();  // S reads done before the PV MMA may overwrite block 0
             mbar_arrive(&p_full[pst]);
             TRACE(14);
@@ -680,12 +712,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       named_bar_sync(1, 256);
       for (int qt = 0; qt < L.n_qt; ++qt, ++tcnt) {
-        const float mx = pass1(tcnt);
+        const float mx = pass1(tcnt, qt);
         if (pend) {
           epilogue(pend_t, pend_row, pend_h, pend_qt, pend_inv);
           pend = false;
         }
-        const float inv = pass2(tcnt, mx);
+        const float inv = pass2(tcnt, mx, qt);
         if (L.n_s == 2) {
           pend = true;
           pend_t = tcnt;

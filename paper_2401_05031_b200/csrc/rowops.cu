@@ -11,58 +11,110 @@ namespace ta {
 
 // ------------------------------------------------------------------ patchify
 // out[b*Np + py*G + px, c*P*P + ky*P + kx] = img[b, c, py*P + ky, px*P + kx]; cols >= 3P^2 zero.
-// One CTA per (patch row py, image b): the 3 x P x S input strip is read once, coalesced,
-// into smem; the G x Kp output block is written with consecutive threads on consecutive
-// columns (two elements per thread).
-template <typename T>
-__global__ void __launch_bounds__(256) patchify_kernel(const float* __restrict__ img,
-                                                       T* __restrict__ out, int S, int P, int Kp) {
-  extern __shared__ float strip[];  // [3][P][S]
-  const int py = blockIdx.x, b = blockIdx.y;
-  const int G = S / P;
-  const int K = 3 * P * P;
-  const int n4 = 3 * P * S / 4;
-  for (int i = threadIdx.x; i < n4; i += blockDim.x) {
-    const int e = 4 * i;
-    const int c = e / (P * S), rem = e % (P * S);
-    const int ky = rem / S, x = rem % S;
-    reinterpret_cast<float4*>(strip)[i] = *reinterpret_cast<const float4*>(
-        img + ((static_cast<long long>(b) * 3 + c) * S + py * P + ky) * S + x);
-  }
-  __syncthreads();
-  T* ob = out + (static_cast<long long>(b) * G * G + static_cast<long long>(py) * G) * Kp;
-  const int total2 = G * Kp / 2;
-  for (int i = threadIdx.x; i < total2; i += blockDim.x) {
-    float v[2];
+// One thread per (patch, c, ky) segment: P consecutive input floats (64 B at P = 16) straight
+// from HBM in registers, P consecutive output elements written back.  Consecutive threads own
+// consecutive (c, ky) of one patch, so a warp's stores are one contiguous run of the output row
+// and every input byte is read once; one integer division per P elements (the previous
+// element-wise im2col spent most of its time in runtime divisions).
+template <int kP, typename T>
+__device__ __forceinline__ void patch_segment(const float* __restrict__ src, T* __restrict__ dst) {
+  float v[kP];
+  if constexpr (kP % 4 == 0) {
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int idx = 2 * i + u;
-      const int px = idx / Kp, col = idx % Kp;
-      float val = 0.f;
-      if (col < K) {
-        const int c = col / (P * P), rem = col % (P * P);
-        const int ky = rem / P, kx = rem % P;
-        val = strip[(c * P + ky) * S + px * P + kx];
-      }
-      v[u] = val;
+    for (int i = 0; i < kP / 4; ++i) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(src) + i);
+      v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
     }
-    if constexpr (sizeof(T) == 2)
-      reinterpret_cast<uint32_t*>(ob)[i] = pack_bf16(v[0], v[1]);
-    else
-      reinterpret_cast<float2*>(ob)[i] = make_float2(v[0], v[1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kP / 2; ++i) {
+      const float2 q = __ldg(reinterpret_cast<const float2*>(src) + i);
+      v[2 * i] = q.x; v[2 * i + 1] = q.y;
+    }
   }
+  if constexpr (sizeof(T) == 2) {
+    uint32_t w[kP / 2];
+#pragma unroll
+    for (int i = 0; i < kP / 2; ++i) w[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+    if constexpr (kP % 8 == 0) {
+#pragma unroll
+      for (int i = 0; i < kP / 8; ++i)
+        reinterpret_cast<uint4*>(dst)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < kP / 2; ++i) reinterpret_cast<uint32_t*>(dst)[i] = w[i];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kP / 2; ++i)
+      reinterpret_cast<float2*>(dst)[i] = make_float2(v[2 * i], v[2 * i + 1]);
+  }
+}
+
+// kP = 0: runtime patch size (scalar copies); kP = 14 / 16: the ViT-H/14 and ViT-B,L/16 cases.
+template <int kP, typename T>
+__global__ void __launch_bounds__(256) patchify_kernel(const float* __restrict__ img,
+                                                       T* __restrict__ out, int B, int S, int P_rt,
+                                                       int Kp) {
+  const int P = kP ? kP : P_rt;
+  const int G = S / P, segs = 3 * P;
+  const int n = B * G * G * segs;  // < 2^31 (checked by the launcher)
+  grid_dep_wait();
+  grid_dep_launch();
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
+    const int patch = idx / segs;  // b * G * G + py * G + px
+    const int seg = idx - patch * segs;  // c * P + ky
+    const int b = patch / (G * G);
+    const int pp = patch - b * G * G;
+    const int py = pp / G, px = pp - py * G;
+    const int c = seg / P, ky = seg - c * P;
+    const float* src = img + ((static_cast<long long>(b) * 3 + c) * S + py * P + ky) * S + px * P;
+    T* row = out + static_cast<long long>(patch) * Kp;
+    T* dst = row + seg * P;
+    if constexpr (kP != 0) {
+      patch_segment<kP, T>(src, dst);
+    } else {
+      for (int kx = 0; kx < P; ++kx) dst[kx] = static_cast<T>(__ldg(src + kx));
+    }
+    if (seg == 0)  // zero padding columns [3P^2, Kp)
+      for (int col = 3 * P * P; col < Kp; ++col) row[col] = static_cast<T>(0.f);
+  }
+}
+
+template <int kP>
+static cudaError_t launch_patchify(const float* img, void* out, int B, int S, int P, int Kp,
+                                   int dtype, cudaStream_t s) {
+  const long long n = static_cast<long long>(B) * (S / P) * (S / P) * 3 * P;
+  const long long want = (n + 255) / 256;
+  const int grid = static_cast<int>(want < 148LL * 16 ? want : 148LL * 16);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (dtype == TA_DTYPE_BF16)
+    return cudaLaunchKernelEx(&cfg, patchify_kernel<kP, __nv_bfloat16>, img,
+                              static_cast<__nv_bfloat16*>(out), B, S, P, Kp);
+  return cudaLaunchKernelEx(&cfg, patchify_kernel<kP, float>, img, static_cast<float*>(out), B, S,
+                            P, Kp);
 }
 
 int patchify(const float* img, void* out, int B, int S, int P, int Kp, int dtype,
              cudaStream_t s) {
-  if (S % 4 != 0 || Kp % 2 != 0) return TA_ERR_SHAPE;
-  const size_t smem = static_cast<size_t>(3) * P * S * sizeof(float);
-  dim3 grid(S / P, B);
-  if (dtype == TA_DTYPE_BF16)
-    patchify_kernel<__nv_bfloat16><<<grid, 256, smem, s>>>(img, static_cast<__nv_bfloat16*>(out), S, P, Kp);
+  if (S % P != 0 || Kp < 3 * P * P ||
+      static_cast<long long>(B) * (S / P) * (S / P) * 3 * P >= (1LL << 31))
+    return TA_ERR_SHAPE;
+  cudaError_t e;
+  if (P == 16 && S % 4 == 0)
+    e = launch_patchify<16>(img, out, B, S, P, Kp, dtype, s);
+  else if (P == 14 && S % 2 == 0)
+    e = launch_patchify<14>(img, out, B, S, P, Kp, dtype, s);
   else
-    patchify_kernel<float><<<grid, 256, smem, s>>>(img, static_cast<float*>(out), S, P, Kp);
-  cudaError_t e = cudaGetLastError();
+    e = launch_patchify<0>(img, out, B, S, P, Kp, dtype, s);
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 

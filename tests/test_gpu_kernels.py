@@ -125,6 +125,24 @@ def test_attention(L, t, hd, heads, with_size, dtype):
         torch.testing.assert_close(out.double(), ref, rtol=1e-5, atol=1e-5)
 
 
+@pytest.mark.parametrize("t", [5, 21, 101, 133, 197, 213, 389])
+@pytest.mark.parametrize("with_size", [False, True])
+def test_attention_batched_tails(L, t, with_size):
+    """bf16 tcgen05 path with many images: padded keys of a tile are the next image's rows
+    (or TMA zero fill), idle row warps and the trimmed last key block must not leak."""
+    b, heads, hd = 24, 12, 64
+    g = torch.Generator(device="cuda").manual_seed(1000 + t)
+    qkv = (torch.randn(b, t, 3 * heads * hd, device="cuda", generator=g) * 2).bfloat16()
+    size = (torch.randint(1, 9, (b, t), device="cuda", generator=g).float() if with_size else None)
+    out = torch.empty(b, t, heads * hd, device="cuda", dtype=torch.bfloat16)
+    _chk(L.ta_attention(qkv.data_ptr(), size.data_ptr() if size is not None else None, b, t, heads, hd,
+                        out.data_ptr(), 0, _s()))
+    torch.cuda.synchronize()
+    ref = _attn_ref(qkv.float(), size, b, t, heads, hd)
+    assert torch.isfinite(out.float()).all()
+    torch.testing.assert_close(out.double(), ref, rtol=2e-2, atol=2e-2)
+
+
 @pytest.mark.parametrize("t,r", [(197, 8), (197, 16), (189, 8), (21, 10), (3, 1), (257, 24), (4, 1)])
 @pytest.mark.parametrize("c", [64, 80])
 def test_match_bit_exact(L, t, r, c):
