@@ -294,13 +294,16 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// 0 = tcgen05 kernel where it applies (default), 1 = force the mma.sync kernel
-// (TA_ATTENTION_BACKEND=mma; used by the parity tests to cover both kernels).
+// 0 = default, by measured speed (tools/attn_bench.py, B = 256, H = 12, hd = 64): the mma.sync
+// kernel for t <= 64 (one 64-row query tile: 24.7 vs 37.4 us at t = 53), the whole-row tcgen05
+// kernel (attention_tc.cu) for 64 < t <= 512 (117 vs 213 / 239 us at t = 197), the chunk-
+// pipelined tcgen05 kernel (attention_fa.cu) beyond (1420 vs 1771 us at t = 581, H = 16).
+// TA_ATTENTION_BACKEND=tc / fa / mma forces one kernel (the parity tests cover all three).
 static int attention_backend() {
   static int mode = -1;
   if (mode < 0) {
     const char* v = getenv("TA_ATTENTION_BACKEND");
-    mode = (v && v[0] == 'm') ? 1 : 0;
+    mode = !v ? 0 : v[0] == 'm' ? 1 : v[0] == 't' ? 2 : v[0] == 'f' ? 3 : 0;
   }
   return mode;
 }
@@ -309,9 +312,12 @@ int attention(const void* qkv, const float* size, int B, int t, int H, int hd, v
               int dtype, cudaStream_t s) {
   if (t <= 0) return TA_OK;
   cudaError_t e;
-  if (dtype == TA_DTYPE_BF16 && attention_backend() == 0) {
-    const int rc = attention_tc(qkv, size, B, t, H, hd, out, s);
-    if (rc != TA_ERR_SHAPE) return rc;  // outside the tcgen05 envelope -> mma.sync below
+  const int backend = attention_backend();
+  if (dtype == TA_DTYPE_BF16 && backend != 1 && !(backend == 0 && t <= 64)) {
+    int rc = TA_ERR_SHAPE;
+    if (backend == 2 || (backend == 0 && t <= 512)) rc = attention_tc(qkv, size, B, t, H, hd, out, s);
+    if (rc == TA_ERR_SHAPE && backend != 2) rc = attention_fa(qkv, size, B, t, H, hd, out, s);
+    if (rc != TA_ERR_SHAPE) return rc;  // outside the tcgen05 envelopes -> mma.sync below
   }
   if (dtype == TA_DTYPE_BF16) {
     cudaLaunchConfig_t cfg = {};

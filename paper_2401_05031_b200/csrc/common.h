@@ -107,6 +107,8 @@ int merge(const float* x, const float* size, int B, int t, int D, int r, const i
 // attention.cu / attention_tc.cu
 int attention_tc(const void* qkv, const float* size, int B, int t, int H, int hd, void* out,
                  cudaStream_t s);
+int attention_fa(const void* qkv, const float* size, int B, int t, int H, int hd, void* out,
+                 cudaStream_t s);
 int attention(const void* qkv, const float* size, int B, int t, int H, int hd, void* out,
               int dtype, cudaStream_t s);
 

@@ -57,6 +57,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Blocking wait that lets the thread sleep (up to hint_ns per try) instead of spinning: for
+// producer threads, whose spin loops otherwise take issue slots from the compute warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t hint_ns = 2000) {
+  const uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(addr),
+      "r"(parity), "r"(hint_ns)
+      : "memory");
+}
+
 // Non-blocking probe: has the phase with this parity completed?
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;

@@ -1,0 +1,47 @@
+"""Subprocess body of tests/test_gpu_attention_backends.py: the attention backend is chosen
+once per process from TA_ATTENTION_BACKEND, so each backend is checked in its own process.
+Prints one line per shape and exits non-zero on the first mismatch."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2401_05031_b200 import _cuda  # noqa: E402
+
+
+def ref(qkv, size, b, t, heads, hd):
+    x = qkv.double().reshape(b, t, 3, heads, hd).permute(2, 0, 3, 1, 4)
+    s = (x[0] @ x[1].transpose(-2, -1)) * hd ** -0.5
+    if size is not None:
+        s = s + size.double().log()[:, None, None, :]
+    return (s.softmax(-1) @ x[2]).transpose(1, 2).reshape(b, t, heads * hd)
+
+
+def main():
+    lib = _cuda.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    shapes = [(7, 1), (5, 33), (6, 64), (4, 65), (3, 197), (2, 300), (2, 513), (2, 581)]
+    for b, t in shapes:
+        for with_size in (False, True):
+            heads, hd = 12, 64
+            g = torch.Generator(device="cuda").manual_seed(t * 31 + b)
+            qkv = (torch.randn(b, t, 3 * heads * hd, device="cuda", generator=g) * 1.5).bfloat16()
+            size = torch.randint(1, 7, (b, t), device="cuda", generator=g).float() if with_size else None
+            out = torch.empty(b, t, heads * hd, device="cuda", dtype=torch.bfloat16)
+            _cuda.check(lib.ta_attention(qkv.data_ptr(), size.data_ptr() if size is not None else None,
+                                         b, t, heads, hd, out.data_ptr(), 0, st))
+            torch.cuda.synchronize()
+            r = ref(qkv.float(), size, b, t, heads, hd)
+            # bf16 output: |err| <= 2e-2 + 2e-2 |ref| (torch.testing.assert_close form)
+            excess = ((out.double() - r).abs() - (2e-2 + 2e-2 * r.abs())).max().item()
+            err = (out.double() - r).abs().max().item()
+            print(f"{os.environ.get('TA_ATTENTION_BACKEND', 'default')} b={b} t={t} size={with_size} "
+                  f"max|err|={err:.3e} excess={excess:.3e}")
+            if not excess <= 0:
+                sys.exit(1)
+
+
+if __name__ == "__main__":
+    main()

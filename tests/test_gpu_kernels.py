@@ -127,12 +127,19 @@ def test_attention(L, t, hd, heads, with_size, dtype):
 
 @pytest.mark.parametrize("t", [5, 21, 101, 133, 197, 213, 389])
 @pytest.mark.parametrize("with_size", [False, True])
-def test_attention_batched_tails(L, t, with_size):
+@pytest.mark.parametrize("ramp", [False, True])
+def test_attention_batched_tails(L, t, with_size, ramp):
     """bf16 tcgen05 path with many images: padded keys of a tile are the next image's rows
-    (or TMA zero fill), idle row warps and the trimmed last key block must not leak."""
+    (or TMA zero fill), idle row warps and the trimmed last key block must not leak.  ramp:
+    key norms grow with the key index, so later key chunks raise the row max far above the
+    first chunk's (the lazy-rescale path of attention_fa.cu)."""
     b, heads, hd = 24, 12, 64
     g = torch.Generator(device="cuda").manual_seed(1000 + t)
-    qkv = (torch.randn(b, t, 3 * heads * hd, device="cuda", generator=g) * 2).bfloat16()
+    qkv = torch.randn(b, t, 3 * heads * hd, device="cuda", generator=g) * 2
+    if ramp:
+        D = heads * hd
+        qkv[:, :, D:2 * D] *= torch.linspace(0.1, 3.0, t, device="cuda")[None, :, None]
+    qkv = qkv.bfloat16()
     size = (torch.randint(1, 9, (b, t), device="cuda", generator=g).float() if with_size else None)
     out = torch.empty(b, t, heads * hd, device="cuda", dtype=torch.bfloat16)
     _chk(L.ta_attention(qkv.data_ptr(), size.data_ptr() if size is not None else None, b, t, heads, hd,

@@ -6,7 +6,8 @@ from paper_2401_05031_b200 import _cuda
 
 lib = _cuda.lib()
 st = torch.cuda.current_stream().cuda_stream
-for B, t, H, hd in [(256, 197, 12, 64), (256, 101, 12, 64), (256, 389, 12, 64), (256, 21, 12, 64), (256, 197, 16, 64)]:
+SHAPES = [tuple(int(v) for v in s.split(",")) for s in os.environ["SHAPES"].split(";")] if os.environ.get("SHAPES") else [(256, 197, 12, 64), (256, 101, 12, 64), (256, 389, 12, 64), (256, 21, 12, 64), (256, 197, 16, 64), (256, 581, 16, 64), (512, 257, 16, 80)]
+for B, t, H, hd in SHAPES:
     qkv = torch.randn(B * t, 3 * H * hd, device="cuda").bfloat16()
     size = torch.ones(B, t, device="cuda")
     out = torch.empty(B * t, H * hd, device="cuda", dtype=torch.bfloat16)
