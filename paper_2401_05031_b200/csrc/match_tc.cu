@@ -1,18 +1,16 @@
 // Bipartite soft matching on the tensor cores (north_star 1).
 //
-//   metric_split_kernel  metric = mean over heads of k (fixed head order), x / ||x||_2, then a
-//                        3xTF32 split x = hi + lo (hi = x truncated to tf32, lo = x - hi) for the
-//                        alternating sets A = even tokens (cls first) and B = odd tokens.
-//                        Layout: scratch[b][part][128][cp] fp32, part = A_hi, A_lo, B_hi, B_lo,
-//                        rows past the set size and columns past c are zero.
-//   match_tc_kernel      TMA loads the four 128 x cp tiles (SW128, K-major, 32-float boxes),
-//                        one thread issues S = A_hi B_hi^T + A_hi B_lo^T + A_lo B_hi^T as
-//                        tcgen05.mma kind::tf32 (M = N = 128, K = 8) into TMEM; thread i owns
-//                        A row i (TMEM lane i) and takes its max / argmax over the B columns
-//                        straight from tcgen05.ld registers (ties -> lowest column; row 0 is
-//                        the class token -> -inf); top-r by rank counting
-//                        rank_i = #{j : v_j > v_i or (v_j == v_i and j < i)} (stable descending
-//                        order), unm = remaining rows ascending.
+//   match_fused_kernel   one CTA per image: metric = mean over heads of k (fixed head order),
+//                        x / ||x||_2, 3xTF32 split x = hi + lo (hi = x truncated to tf32, lo =
+//                        x - hi) for the alternating sets A = even tokens (cls first) and B =
+//                        odd tokens, written straight into SW128 K-major smem tiles; one thread
+//                        issues S = A_hi B_hi^T + A_hi B_lo^T + A_lo B_hi^T as tcgen05.mma
+//                        kind::tf32 (M = N = 128, K = 8) into TMEM; thread i owns A row i (TMEM
+//                        lane i) and takes its max / argmax over the B columns straight from
+//                        tcgen05.ld registers (ties -> lowest column; row 0 is the class token
+//                        -> -inf); top-r by rank counting rank_i = #{j : v_j > v_i or (v_j ==
+//                        v_i and j < i)} (stable descending order), unm = remaining rows
+//                        ascending.  (k is read once; no global scratch round trip.)
 // The 3xTF32 contraction is accurate to ~1e-6 relative, the level of an fp32 dot product.
 #include <cfloat>
 
@@ -31,128 +29,195 @@ __device__ __forceinline__ float tf32_trunc(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
-// grid (B, 8), block 256: one warp per token row, 32 rows per CTA.  Each lane owns column
-// pairs (2 lane, 2 lane + 1) (+64): all heads' k values are loaded before the sum, in head
-// order, so the fixed summation order of the SIMT kernel is kept.
-template <typename QT>
-__global__ void __launch_bounds__(256)
-    metric_split_kernel(const float* __restrict__ metric, const QT* __restrict__ qkv, int t,
-                        int heads, int c, int cp, float* __restrict__ scratch) {
-  const int b = blockIdx.x;
-  const int na = (t + 1) / 2, nb = t / 2;
-  float* base = scratch + static_cast<long long>(b) * 4 * kRows * cp;
-  grid_dep_wait();
-  grid_dep_launch();  // early trigger: the next kernel's prologue overlaps our tail
-  const int lane = lane_id();
-  const int row = blockIdx.y * 32 + warp_id() * 4;
-  for (int rr = row; rr < row + 4; ++rr) {
-    const int set = rr / kRows;  // 0 = A (even tokens), 1 = B (odd tokens)
-    const int ri = rr % kRows;
-    const int tok = 2 * ri + set;
-    const bool valid = ri < (set ? nb : na);
-    float* hi = base + (static_cast<long long>(set * 2) * kRows + ri) * cp;
-    float* lo = hi + static_cast<long long>(kRows) * cp;
-    float v[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
-    float ss = 0.f;
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int j = 2 * lane + 64 * u;  // columns j, j + 1 (c is even)
-      if (valid && j < c) {
-        if (metric != nullptr) {
-          const float2 m2 = *reinterpret_cast<const float2*>(
-              metric + (static_cast<long long>(b) * t + tok) * c + j);
-          v[u][0] = m2.x;
-          v[u][1] = m2.y;
-        } else {
-          const long long D = static_cast<long long>(heads) * c;
-          const QT* kr = qkv + (static_cast<long long>(b) * t + tok) * 3 * D + D + j;
-          float2 kv[16];
-#pragma unroll
-          for (int h = 0; h < 16; ++h) {
-            if (h < heads) {
-              if constexpr (sizeof(QT) == 2)
-                kv[h] = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(kr + h * c));
-              else
-                kv[h] = *reinterpret_cast<const float2*>(kr + h * c);
-            }
-          }
-          float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-          for (int h = 0; h < 16; ++h) {
-            if (h < heads) {
-              a0 += kv[h].x;
-              a1 += kv[h].y;
-            }
-          }
-          v[u][0] = a0 / heads;
-          v[u][1] = a1 / heads;
-        }
-      }
-      ss += v[u][0] * v[u][0] + v[u][1] * v[u][1];
-    }
-    const float nrm = sqrtf(warp_sum(ss));
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int j = 2 * lane + 64 * u;
-      if (j < cp) {
-        float2 h2, l2;
-        const float x0 = valid ? v[u][0] / nrm : 0.f;
-        const float x1 = valid ? v[u][1] / nrm : 0.f;
-        h2.x = tf32_trunc(x0);
-        h2.y = tf32_trunc(x1);
-        l2.x = tf32_trunc(x0 - h2.x);
-        l2.y = tf32_trunc(x1 - h2.y);
-        *reinterpret_cast<float2*>(hi + j) = h2;
-        *reinterpret_cast<float2*>(lo + j) = l2;
-      }
-    }
-  }
-}
+constexpr int kFusedThreads = 512;
 
-__global__ void __launch_bounds__(128, 1)
-    match_tc_kernel(const __grid_constant__ CUtensorMap tm, int t, int cp, int r,
-                    int32_t* __restrict__ src_out, int32_t* __restrict__ dst_out,
-                    int32_t* __restrict__ unm_out) {
+// One CTA per image, 16 warps.  Phase 1 (all warps): metric row of every token (mean over
+// heads of k in fixed head order, or the given fp32 metric), x / ||x||_2, 3xTF32 split
+// x = hi + lo, written straight into the four SW128 K-major smem tiles the MMA reads (A_hi,
+// A_lo, B_hi, B_lo: 128 rows x cp floats, 32-float chunks of 128-byte rows, 16-byte chunk c of
+// row i at slot c ^ (i & 7)); pad columns c..cp are zero.  Rows past a set's size are never
+// read by the selection (their S rows / columns are masked), so they are not cleared.
+// Phase 2 (thread 0): S = A_hi B_hi^T + A_hi B_lo^T + A_lo B_hi^T, kind::tf32 into TMEM.
+// Phase 3 (warps 0..3, thread i = A row i = TMEM lane i): max / argmax over the B columns
+// (ties -> lowest column; the class token row is -inf), top-r by rank counting, unm ascending.
+template <typename QT, int kU>  // kU: 64-column passes per row (1: c <= 64, 2: c <= 128)
+__global__ void __launch_bounds__(kFusedThreads, 1)
+    match_fused_kernel(const float* __restrict__ metric, const QT* __restrict__ qkv, int t,
+                       int heads, int c, int cp, int r, int32_t* __restrict__ src_out,
+                       int32_t* __restrict__ dst_out, int32_t* __restrict__ unm_out) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   const int b = blockIdx.x;
   const int na = (t + 1) / 2, nb = t / 2;
-  const int nkc = cp / 32;                  // 32-float K chunks (128-byte swizzle rows)
+  const int nkc = cp / 32;                   // 32-float K chunks (128-byte swizzle rows)
   const int tile_bytes = nkc * kRows * 128;  // one part
   float* node_max = reinterpret_cast<float*>(smem + 4 * tile_bytes);
   int* node_idx = reinterpret_cast<int*>(node_max + kRows);
   int* rank = node_idx + kRows;
-  uint64_t* bar_ld = reinterpret_cast<uint64_t*>(rank + kRows);
-  uint64_t* bar_mma = bar_ld + 1;
+  uint64_t* bar_mma = reinterpret_cast<uint64_t*>(rank + kRows);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_mma + 1);
-  const int i = threadIdx.x;
-  const uint32_t warp = warp_id();
+  const int tid = threadIdx.x;
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t s0 = smem_u32(smem);
 
-  if (i == 0) {
-    tma_prefetch(&tm);
-    mbar_init(bar_ld, 1);
+  if (tid == 0) {
     mbar_init(bar_mma, 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<128>(tmem_slot);
+  grid_dep_wait();    // qkv comes from the previous kernels
+  grid_dep_launch();  // early trigger: the next kernel's prologue overlaps our tail
+
+  // ---- phase 1: metric rows -> normalised, split, swizzled smem tiles
+  const long long D = static_cast<long long>(heads) * c;
+  if constexpr (sizeof(QT) == 2) {
+    if (metric == nullptr) {
+      // bf16 k: a warp covers a row pair (lanes 0..15 the even token -> set A, 16..31 the odd
+      // one -> set B), 4 columns (8 bytes) per lane and head; two pairs per iteration with
+      // every head's load issued before the head-order sums, so ~6 KB per warp are in flight.
+      const int sub = static_cast<int>(lane) >> 4;
+      const int cl = (static_cast<int>(lane) & 15) * 4;
+      const int n_pairs = (t + 1) / 2;
+      for (int p0 = static_cast<int>(warp); p0 < n_pairs; p0 += 2 * (kFusedThreads / 32)) {
+        uint2 raw[2][kU][16];
+#pragma unroll
+        for (int pp = 0; pp < 2; ++pp) {
+          const int tok = 2 * (p0 + pp * (kFusedThreads / 32)) + sub;
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int j = cl + 64 * u;
+            if (tok < t && j < c) {
+              const QT* kr = qkv + (static_cast<long long>(b) * t + tok) * 3 * D + D + j;
+#pragma unroll
+              for (int hh = 0; hh < 16; ++hh)
+                if (hh < heads) raw[pp][u][hh] = __ldg(reinterpret_cast<const uint2*>(kr + hh * c));
+            }
+          }
+        }
+#pragma unroll
+        for (int pp = 0; pp < 2; ++pp) {
+          const int tok = 2 * (p0 + pp * (kFusedThreads / 32)) + sub;
+          float v[kU][4];
+          float ss = 0.f;
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int j = cl + 64 * u;
+            float a[4] = {0.f, 0.f, 0.f, 0.f};
+            if (tok < t && j < c) {
+#pragma unroll
+              for (int hh = 0; hh < 16; ++hh) {
+                if (hh < heads) {
+                  const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw[pp][u][hh].x));
+                  const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw[pp][u][hh].y));
+                  a[0] += lo.x;
+                  a[1] += lo.y;
+                  a[2] += hi.x;
+                  a[3] += hi.y;
+                }
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              v[u][e] = a[e] / heads;
+              ss += v[u][e] * v[u][e];
+            }
+          }
+          // norm over the 16 lanes of this row
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+          const float nrm = sqrtf(ss);
+          if (tok < t) {
+            const int ri = tok >> 1;
+            const uint32_t row_hi = s0 + (sub * 2) * tile_bytes + ri * 128;
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              const int j = cl + 64 * u;
+              if (j < cp) {
+                float hv[4], lv[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float x = j + e < c ? v[u][e] / nrm : 0.f;
+                  hv[e] = tf32_trunc(x);
+                  lv[e] = tf32_trunc(x - hv[e]);
+                }
+                const int kc = j >> 5, jj = j & 31;
+                const uint32_t off = kc * kRows * 128 + (((jj >> 2) ^ (ri & 7)) << 4);
+                sts_f4(row_hi + off, make_float4(hv[0], hv[1], hv[2], hv[3]));
+                sts_f4(row_hi + tile_bytes + off, make_float4(lv[0], lv[1], lv[2], lv[3]));
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  if (sizeof(QT) == 4 || metric != nullptr) {
+    for (int tok = static_cast<int>(warp); tok < t; tok += kFusedThreads / 32) {
+      float v[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+      float ss = 0.f;
+  #pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int j = 2 * static_cast<int>(lane) + 64 * u;  // columns j, j + 1 (c is even)
+        if (j < c) {
+          if (metric != nullptr) {
+            const float2 m2 = *reinterpret_cast<const float2*>(metric + (static_cast<long long>(b) * t + tok) * c + j);
+            v[u][0] = m2.x;
+            v[u][1] = m2.y;
+          } else {
+            const QT* kr = qkv + (static_cast<long long>(b) * t + tok) * 3 * D + D + j;
+            float2 kv[16];
+  #pragma unroll
+            for (int hh = 0; hh < 16; ++hh) {
+              if (hh < heads) {
+                if constexpr (sizeof(QT) == 2)
+                  kv[hh] = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(kr + hh * c));
+                else
+                  kv[hh] = *reinterpret_cast<const float2*>(kr + hh * c);
+              }
+            }
+            float a0 = 0.f, a1 = 0.f;
+  #pragma unroll
+            for (int hh = 0; hh < 16; ++hh) {
+              if (hh < heads) {
+                a0 += kv[hh].x;
+                a1 += kv[hh].y;
+              }
+            }
+            v[u][0] = a0 / heads;
+            v[u][1] = a1 / heads;
+          }
+        }
+        ss += v[u][0] * v[u][0] + v[u][1] * v[u][1];
+      }
+      const float nrm = sqrtf(warp_sum(ss));
+      const int set = tok & 1, ri = tok >> 1;
+      const uint32_t row_hi = s0 + (set * 2) * tile_bytes + ri * 128;
+  #pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int j = 2 * static_cast<int>(lane) + 64 * u;
+        if (j < cp) {
+          const float x0 = j < c ? v[u][0] / nrm : 0.f;
+          const float x1 = j < c ? v[u][1] / nrm : 0.f;
+          const float h0 = tf32_trunc(x0), h1 = tf32_trunc(x1);
+          const float l0 = tf32_trunc(x0 - h0), l1 = tf32_trunc(x1 - h1);
+          const int kc = j >> 5, jj = j & 31;
+          const uint32_t off = kc * kRows * 128 + ((((jj >> 2) ^ (ri & 7))) << 4) + (jj & 3) * 4;
+          asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(row_hi + off), "f"(h0), "f"(h1) : "memory");
+          asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(row_hi + tile_bytes + off), "f"(l0), "f"(l1) : "memory");
+        }
+      }
+    }
+  }
+  fence_proxy_async_shared();  // generic-proxy tile writes -> visible to the MMA (async proxy)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  grid_dep_wait();  // scratch comes from metric_split_kernel
-  grid_dep_launch();  // early trigger: the next kernel's prologue overlaps our tail
 
-  if (i == 0) {
-    mbar_arrive_expect_tx(bar_ld, 4 * tile_bytes);
-    for (int part = 0; part < 4; ++part)
-      for (int kc = 0; kc < nkc; ++kc)
-        tma_load_2d(&tm, bar_ld, smem + part * tile_bytes + kc * kRows * 128, kc * 32,
-                    (b * 4 + part) * kRows);
-    mbar_wait(bar_ld, 0);
-    tc_fence_after();
+  // ---- phase 2: S = A B^T in 3xTF32
+  if (tid == 0) {
     constexpr uint32_t idesc = idesc_tf32(kRows, kRows);
-    const uint32_t s0 = smem_u32(smem);
     // (A part, B part): hi*hi, hi*lo, lo*hi
     const int terms[3][2] = {{0, 2}, {0, 3}, {1, 2}};
     int n = 0;
@@ -167,34 +232,37 @@ __global__ void __launch_bounds__(128, 1)
     }
     umma_commit(bar_mma);
   }
-  __syncwarp();
-  mbar_wait(bar_mma, 0);
-  tc_fence_after();
-
-  // row max / argmax of S[i, 0..nb) from TMEM (thread i = lane i)
-  float best = -INFINITY;
-  int best_j = 0;
-  const uint32_t la = tmem + ((warp * 32u) << 16);
-  for (int c0 = 0; c0 < kRows; c0 += 32) {
-    uint32_t v[32];
-    tmem_ld_32x32b_x32(la + c0, v);
-    tmem_ld_wait();
-    if (i > 0) {
+  if (warp < 4) {
+    const int i = tid;
+    __syncwarp();
+    mbar_wait(bar_mma, 0);
+    tc_fence_after();
+    // ---- phase 3: row max / argmax of S[i, 0..nb) from TMEM (thread i = lane i)
+    float best = -INFINITY;
+    int best_j = 0;
+    const uint32_t la = tmem + ((warp * 32u) << 16);
+    for (int c0 = 0; c0 < kRows; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(la + c0, v);
+      tmem_ld_wait();
+      if (i > 0) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float s = __uint_as_float(v[j]);
-        if (c0 + j < nb && s > best) {  // ascending j, strict >: lowest column on ties
-          best = s;
-          best_j = c0 + j;
+        for (int j = 0; j < 32; ++j) {
+          const float sv = __uint_as_float(v[j]);
+          if (c0 + j < nb && sv > best) {  // ascending j, strict >: lowest column on ties
+            best = sv;
+            best_j = c0 + j;
+          }
         }
       }
     }
+    node_max[i] = i < na ? best : -INFINITY;
+    node_idx[i] = best_j;
   }
-  node_max[i] = i < na ? best : -INFINITY;
-  node_idx[i] = best_j;
   tc_fence_before();
   __syncthreads();
-  if (i < na) {
+  if (tid < na) {
+    const int i = tid;
     const float vi = node_max[i];
     int rk = 0;
     for (int j = 0; j < na; ++j) {
@@ -204,7 +272,8 @@ __global__ void __launch_bounds__(128, 1)
     rank[i] = rk;
   }
   __syncthreads();
-  if (i < na) {
+  if (tid < na) {
+    const int i = tid;
     const int rk = rank[i];
     if (rk < r) {
       src_out[static_cast<long long>(b) * r + rk] = i;
@@ -220,28 +289,6 @@ __global__ void __launch_bounds__(128, 1)
     tc_fence_after();
     tmem_dealloc<128>(tmem);
   }
-}
-
-int make_tmap_f32_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
-                     uint32_t box_cols, uint32_t box_rows) {
-  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-  if (!enc) {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return TA_ERR_CUDA;
-    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * 4};
-  cuuint32_t box[2] = {box_cols, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
-                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return res == CUDA_SUCCESS ? TA_OK : TA_ERR_SHAPE;
 }
 
 template <typename... Args>
@@ -262,37 +309,41 @@ cudaError_t launch_pdl(void (*kern)(Args...), dim3 grid, dim3 block, size_t smem
 
 }  // namespace
 
-size_t match_tc_scratch_bytes(int B, int c) {
-  const int cp = (c + 31) / 32 * 32;
-  return static_cast<size_t>(B) * 4 * kRows * cp * sizeof(float);
-}
+// The fused kernel needs no global scratch; a non-null scratch pointer only selects the
+// tensor-core path in match() (tome.cu), so a token allocation is kept in the workspace.
+size_t match_tc_scratch_bytes(int, int) { return 256; }
 
-// Returns TA_ERR_SHAPE outside the kernel's envelope (t > 256 or c > 96).
+// Returns TA_ERR_SHAPE outside the kernel's envelope (t > 256, c > 96 or > 16 heads).
 int match_tc(const float* metric, const void* qkv, int qkv_dtype, int B, int t, int heads, int c,
              int r, int32_t* src, int32_t* dst, int32_t* unm, float* scratch, cudaStream_t s) {
+  (void)scratch;
   const int na = (t + 1) / 2;
   if (r <= 0 || r > na - 1 || t < 3) return TA_ERR_INVALID;
-  if (t > 2 * kRows || c > 96 || (c & 1) || heads > 16 || scratch == nullptr) return TA_ERR_SHAPE;
+  if (t > 2 * kRows || c > 96 || (c & 1) || heads > 16) return TA_ERR_SHAPE;
   const int cp = (c + 31) / 32 * 32;
-  cudaError_t e;
-  if (metric != nullptr || qkv_dtype == TA_DTYPE_F32)
-    e = launch_pdl(metric_split_kernel<float>, dim3(B, 2 * kRows / 32), dim3(256), 0, s, metric,
-                   static_cast<const float*>(qkv), t, heads, c, cp, scratch);
-  else
-    e = launch_pdl(metric_split_kernel<__nv_bfloat16>, dim3(B, 2 * kRows / 32), dim3(256), 0, s, metric,
-                   static_cast<const __nv_bfloat16*>(qkv), t, heads, c, cp, scratch);
-  if (e != cudaSuccess) return set_last_cuda_error(e);
-  CUtensorMap tm;
-  int rc = make_tmap_f32_2d(&tm, scratch, static_cast<uint64_t>(B) * 4 * kRows, cp, 32, kRows);
-  if (rc) return rc;
   const size_t smem = 4 * (cp / 32) * kRows * 128 + 3 * kRows * 4 + 64 + 1024;
   static bool attr_set = false;
+  cudaError_t e;
   if (!attr_set) {
-    e = cudaFuncSetAttribute(match_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    e = cudaFuncSetAttribute(match_fused_kernel<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(match_fused_kernel<__nv_bfloat16, 1>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(match_fused_kernel<__nv_bfloat16, 2>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return set_last_cuda_error(e);
     attr_set = true;
   }
-  e = launch_pdl(match_tc_kernel, dim3(B), dim3(128), smem, s, tm, t, cp, r, src, dst, unm);
+  if (metric != nullptr || qkv_dtype == TA_DTYPE_F32)
+    e = launch_pdl(match_fused_kernel<float, 2>, dim3(B), dim3(kFusedThreads), smem, s, metric,
+                   static_cast<const float*>(qkv), t, heads, c, cp, r, src, dst, unm);
+  else if (c <= 64)
+    e = launch_pdl(match_fused_kernel<__nv_bfloat16, 1>, dim3(B), dim3(kFusedThreads), smem, s, metric,
+                   static_cast<const __nv_bfloat16*>(qkv), t, heads, c, cp, r, src, dst, unm);
+  else
+    e = launch_pdl(match_fused_kernel<__nv_bfloat16, 2>, dim3(B), dim3(kFusedThreads), smem, s, metric,
+                   static_cast<const __nv_bfloat16*>(qkv), t, heads, c, cp, r, src, dst, unm);
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 
