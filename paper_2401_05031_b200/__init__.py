@@ -2,10 +2,12 @@
 
 Host API (drop-in for the reference's ``tokadapt`` package): ``core``, ``profiles``,
 ``errors`` mirror pkg/src/tokadapt/*.py; ``model`` adds the paper's ServeModel /
-TaskModel / TransformerModel on top of the sm_100a CUDA library (``_cuda``).
+TaskModel / TransformerModel on top of the sm_100a CUDA library (``_cuda``); ``batcher``,
+``adapter``, ``workload`` and ``engine`` are the host-side serving loop (Alg. 1-3) that plans
+gamma per batch and executes it on GPU replicas.
 """
 
-from . import config, core, errors, profiles, weights  # noqa: F401
+from . import adapter, batcher, config, core, engine, errors, profiles, weights, workload  # noqa: F401
 from .config import VIT_CONFIGS, ViTConfig, flops_per_image, token_schedule  # noqa: F401
 
 __version__ = "0.1.0"

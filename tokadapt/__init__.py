@@ -2,13 +2,14 @@
 
 `import tokadapt.core` / `tokadapt.profiles` / `tokadapt.errors` resolve to the B200
 implementation in paper_2401_05031_b200; `tokadapt.model` adds ServeModel / TaskModel /
-TransformerModel (PAPER.md:522-527)."""
+TransformerModel (PAPER.md:522-527); `tokadapt.batcher` / `adapter` / `workload` / `engine`
+are the SPEC.md serving modules (Alg. 1-3, workloads, engine + metrics)."""
 
 import sys as _sys
 
-from paper_2401_05031_b200 import config, core, errors, profiles, weights  # noqa: F401
+from paper_2401_05031_b200 import adapter, batcher, config, core, engine, errors, profiles, weights, workload  # noqa: F401
 
-for _name in ("core", "errors", "profiles", "config", "weights"):
+for _name in ("core", "errors", "profiles", "config", "weights", "batcher", "adapter", "workload", "engine"):
     _sys.modules[f"{__name__}.{_name}"] = getattr(_sys.modules["paper_2401_05031_b200"], _name)
 
 
