@@ -49,8 +49,12 @@ struct GemmEpi {
   int row_off = 0;
   // LayerNorm folding (EPI_*_STATS producers / EPI_LN_* consumers)
   void* xh = nullptr;               // producer: bf16 copy of out, same rows
-  float* stats = nullptr;           // producer: [rows, 2] (sum, sumsq), pre-zeroed, atomics
-  const float* ln_stats = nullptr;  // consumer: [M, 2] stats of the A rows
+  // Row statistics as partials per 128-column block: [rows][stat_slots][2] (sum, sumsq) of
+  // the block's values, plain stores (no atomics, no clearing); producers that see whole rows
+  // store the full sums in slot 0 and zeros elsewhere.  Consumers add the slots in order.
+  float* stats = nullptr;           // producer
+  const float* ln_stats = nullptr;  // consumer: stats of the A rows
+  int stat_slots = 0;               // D / 128
   const float* c1 = nullptr;        // consumer: [N]
   const float* c2 = nullptr;        // consumer: [N]
   float inv_dim = 0.f;              // consumer: 1 / D

@@ -139,8 +139,9 @@ Workspace carve(const ta_model* m, int B, const Schedule& s, char* base) {
   w.dst = reinterpret_cast<int32_t*>(take(rows * 4));
   w.unm = reinterpret_cast<int32_t*>(take(rows * 4));
   w.match_scratch = reinterpret_cast<float*>(take(match_tc_scratch_bytes(B, m->hd)));
-  w.stats[0] = reinterpret_cast<float*>(take(rows * 8));
-  w.stats[1] = reinterpret_cast<float*>(take(rows * 8));
+  // LN-folded path: per-row partial (sum, sumsq) per 128-column block (GemmEpi::stats)
+  w.stats[0] = reinterpret_cast<float*>(take(rows * 8 * (D / 128)));
+  w.stats[1] = reinterpret_cast<float*>(take(rows * 8 * (D / 128)));
   w.total = off;
   return w;
 }
@@ -375,10 +376,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
   const bool fused = m->ln_folded && act == TA_DTYPE_BF16;
   float* const ln1_stats = w.stats[0];
   float* const ln2_stats = w.stats[1];
-  auto zero_stats = [&](float* buf, long long rows) {
-    cudaError_t e = cudaMemsetAsync(buf, 0, static_cast<size_t>(rows) * 8, st);
-    return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
-  };
+  const int stat_slots = D / 128;  // partial row statistics per 128-column block
 
   // ---- patch embedding + cls + layer-0 prompts
   TA_TRY(patchify(images, w.patches, B, d.img, d.patch, m->kp, act, st));
@@ -392,9 +390,9 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
     e.rows_out = s.t[0];
     e.row_off = 1;
     if (fused) {
-      TA_TRY(zero_stats(ln1_stats, static_cast<long long>(B) * s.t[0]));
       e.xh = w.h;
       e.stats = ln1_stats;
+      e.stat_slots = stat_slots;
     }
     TA_TRY(linear(m, w.patches, m->w.patch_w, B * m->n_patches, D, m->kp,
                   fused ? EPI_PATCH_STATS : EPI_PATCH, e, st));
@@ -425,6 +423,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
       e.out = w.qkv;
       if (fused) {
         e.ln_stats = ln1_stats;
+        e.stat_slots = stat_slots;
         e.c1 = static_cast<const float*>(Lw.qkv_c1);
         e.c2 = static_cast<const float*>(Lw.qkv_c2);
         e.inv_dim = 1.0f / D;
@@ -448,9 +447,9 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
       e.resid = w.x[cur];
       e.out = w.x[cur];
       if (fused && r == 0) {
-        TA_TRY(zero_stats(ln2_stats, M));
         e.xh = w.h;
         e.stats = ln2_stats;
+        e.stat_slots = stat_slots;
         TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID_STATS, e, st));
   prof.mark("proj");
       } else {
@@ -496,6 +495,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
       e.out = w.mlp;
       if (fused) {
         e.ln_stats = ln2_stats;
+        e.stat_slots = stat_slots;
         e.c1 = static_cast<const float*>(Lw.fc1_c1);
         e.c2 = static_cast<const float*>(Lw.fc1_c2);
         e.inv_dim = 1.0f / D;
@@ -523,9 +523,9 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         e.out = w.x[cur];
       }
       if (stats) {
-        TA_TRY(zero_stats(ln1_stats, static_cast<long long>(B) * s.t[l + 1]));
         e.xh = w.h;
         e.stats = ln1_stats;
+        e.stat_slots = stat_slots;
       }
       TA_TRY(linear(m, w.mlp, Lw.fc2_w, Mp, D, d.mlp_dim,
                     stats ? EPI_BIAS_RESID_STATS : EPI_BIAS_RESID, e, st));

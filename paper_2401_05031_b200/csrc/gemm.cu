@@ -80,7 +80,13 @@ __device__ __forceinline__ void epi_load(const GemmEpi& e, int M, int N, long lo
     for (int k = 0; k < 8; ++k) {
       const long long m = m_base + row0 + 4 * k;
       if (full || m < M) {
-        const float2 st = __ldg(reinterpret_cast<const float2*>(e.ln_stats) + m);
+        const float2* sp = reinterpret_cast<const float2*>(e.ln_stats) + m * e.stat_slots;
+        float2 st = __ldg(sp);
+        for (int j = 1; j < e.stat_slots; ++j) {
+          const float2 p = __ldg(sp + j);
+          st.x += p.x;
+          st.y += p.y;
+        }
         c.x[k].x = st.x;
         c.x[k].y = st.y;
       }
@@ -88,8 +94,8 @@ __device__ __forceinline__ void epi_load(const GemmEpi& e, int M, int N, long lo
   }
 }
 
-// Per-row (sum, sumsq) partials of the values a warp stores, carried across the chunks of
-// one tile and flushed with one atomic pair per row (EPI_*_STATS).
+// Per-row (sum, sumsq) partials of the values a warp stores, carried across the chunks of one
+// 128-column block and stored into that block's slot (EPI_*_STATS).
 struct RowStats {
   float s[8];
   float q[8];
@@ -99,7 +105,8 @@ __device__ __forceinline__ void rowstats_clear(RowStats& r) {
   for (int k = 0; k < 8; ++k) r.s[k] = r.q[k] = 0.f;
 }
 template <bool kRemap>
-__device__ __forceinline__ void rowstats_flush(const GemmEpi& e, int M, long long m_base, RowStats& r) {
+__device__ __forceinline__ void rowstats_flush(const GemmEpi& e, int M, long long m_base, RowStats& r,
+                                               int slot) {
   const uint32_t lane = lane_id();
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -112,8 +119,7 @@ __device__ __forceinline__ void rowstats_flush(const GemmEpi& e, int M, long lon
     const long long m = m_base + (lane >> 3) + 4 * k;
     if ((lane & 7) == 0 && m < M) {
       const long long orow = kRemap ? epi_out_row(e, m) : m;
-      atomicAdd(e.stats + 2 * orow, s);
-      atomicAdd(e.stats + 2 * orow + 1, q);
+      *reinterpret_cast<float2*>(e.stats + 2 * (orow * e.stat_slots + slot)) = make_float2(s, q);
     }
   }
   rowstats_clear(r);
@@ -371,9 +377,10 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
           if (live) epi_load<EPI>(epi, M, N, m_base, nb + (c + 2) * 32, r0, stage, ca);
         }
         if (live) epi_store<EPI, OutT, kRemap>(epi, M, N, m_base, nb + (c + 1) * 32, cb, rs);
-      }
-      if constexpr (epi_is_stats(EPI)) {
-        if (live) rowstats_flush<kRemap>(epi, M, m_base, rs);
+        if constexpr (epi_is_stats(EPI)) {
+          static_assert((BN / kSplit) % 128 == 0, "stats slots are 128-column blocks");
+          if ((c + 2) % 4 == 0 && live) rowstats_flush<kRemap>(epi, M, m_base, rs, (nb + (c - 2) * 32) / 128);
+        }
       }
       if (++acc == 2) {
         acc = 0;
@@ -565,7 +572,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
         float ln_mu = 0.f, ln_rstd = 0.f;
         if constexpr (epi_is_ln(EPI)) {
           if (row_ok) {
-            const float2 st = __ldg(reinterpret_cast<const float2*>(epi.ln_stats) + m);
+            const float2* sp = reinterpret_cast<const float2*>(epi.ln_stats) + m * epi.stat_slots;
+            float2 st = __ldg(sp);
+            for (int j = 1; j < epi.stat_slots; ++j) {
+              const float2 p = __ldg(sp + j);
+              st.x += p.x;
+              st.y += p.y;
+            }
             ln_mu = st.x * epi.inv_dim;
             ln_rstd = rsqrtf(fmaxf(st.y * epi.inv_dim - ln_mu * ln_mu, 0.f) + 1e-6f);
           }
@@ -717,10 +730,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           if (compute(c, w)) stage_store(c, w);
         }
         if constexpr (epi_is_stats(EPI)) {
-          if (row_ok && !epi.skip) {
-            atomicAdd(epi.stats + 2 * orow, st_s);
-            atomicAdd(epi.stats + 2 * orow + 1, st_q);
-          }
+          static_assert(BN / kSplit == 128, "one stats slot per warp and tile");
+          if (row_ok && !epi.skip)
+            *reinterpret_cast<float2*>(epi.stats + 2 * (orow * epi.stat_slots + (n_blk * BN + col0) / 128)) =
+                make_float2(st_s, st_q);
         }
       } else {
         uint32_t r0[32], r1[32];
@@ -753,7 +766,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           if (live) epi_store<EPI, OutT, kRemap>(epi, M, N, m_base, nb + (c + 1) * 32, cb, rs);
         }
         if constexpr (epi_is_stats(EPI)) {
-          if (live) rowstats_flush<kRemap>(epi, M, m_base, rs);
+          if (live) rowstats_flush<kRemap>(epi, M, m_base, rs, nb / 128);
         }
       }
       if (++acc == 2) {

@@ -127,7 +127,7 @@ __global__ void insert_rows_kernel(float* __restrict__ x, int t_total, int D,
                                    const float* const* __restrict__ prompt_tab,
                                    const int32_t* __restrict__ task_ids, int layer, int gamma,
                                    int prompt_row, __nv_bfloat16* __restrict__ xh,
-                                   float* __restrict__ stats) {
+                                   float* __restrict__ stats, int stat_slots) {
   // One warp per inserted row; with xh / stats (LayerNorm folded into the QKV GEMM) the
   // row is also written as bf16 and its exact (sum, sumsq) stored.
   const int b = blockIdx.x;
@@ -163,7 +163,10 @@ __global__ void insert_rows_kernel(float* __restrict__ x, int t_total, int D,
     if (stats != nullptr) {
       s = warp_sum(s);
       q = warp_sum(q);
-      if (lane == 0) *reinterpret_cast<float2*>(stats + 2 * row) = make_float2(s, q);
+      // whole-row sums in slot 0, the other 128-column slots zero (common.h GemmEpi::stats)
+      if (lane < stat_slots)
+        *reinterpret_cast<float2*>(stats + 2 * (row * stat_slots + lane)) =
+            lane == 0 ? make_float2(s, q) : make_float2(0.f, 0.f);
     }
   }
 }
@@ -173,7 +176,8 @@ int insert_rows(float* x, int B, int t_total, int D, const float* cls, const flo
                 int prompt_row, cudaStream_t s, void* xh, float* stats) {
   if (D % 128 != 0) return TA_ERR_SHAPE;
   insert_rows_kernel<<<B, 256, 0, s>>>(x, t_total, D, cls, pos, prompt_tab, task_ids, layer,
-                                       gamma, prompt_row, static_cast<__nv_bfloat16*>(xh), stats);
+                                       gamma, prompt_row, static_cast<__nv_bfloat16*>(xh), stats,
+                                       D / 128);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }

@@ -267,7 +267,10 @@ __global__ void __launch_bounds__(256)
         *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(h_out) + orow * D + cidx) = p;
       }
       const float s_all = warp_sum(sum), q_all = warp_sum(q2);
-      if (lane == 0) *reinterpret_cast<float2*>(stats_out + 2 * orow) = make_float2(s_all, q_all);
+      // whole-row sums in slot 0, the other 128-column slots zero (common.h GemmEpi::stats)
+      if (lane < D / 128)
+        *reinterpret_cast<float2*>(stats_out + 2 * (orow * (D / 128) + lane)) =
+            lane == 0 ? make_float2(s_all, q_all) : make_float2(0.f, 0.f);
       continue;
     }
     // fused LN2

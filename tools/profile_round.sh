@@ -17,6 +17,6 @@ for shape in qkv proj fc1 fc2; do
 done
 T=197 timeout 200 $NCU --set full --import-source on -k regex:attn_tc -s 2 -c 1 \
   -o $OUT/prof_${TAG}_attn_t197 -f python tools/attn_one.py > /dev/null 2>&1
-timeout 200 $NCU --set full --import-source on -k regex:"merge_kernel|metric_split|match_tc|layernorm" -s 8 -c 4 \
+timeout 200 $NCU --set full --import-source on -k regex:"merge_kernel|match_fused|layernorm|patchify" -s 6 -c 3 \
   -o $OUT/prof_${TAG}_tome -f python tools/tome_one.py > /dev/null 2>&1
 ls -la $OUT | grep prof_${TAG}
