@@ -353,7 +353,7 @@ def main():
     ap.add_argument("--cpu-batch", type=int, default=8)
     ap.add_argument("--ref-batch", type=int, default=4)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--fold-ln", type=int, default=0, help="fold LayerNorm into the QKV / fc1 GEMMs")
+    ap.add_argument("--fold-ln", type=int, default=1, help="fold LayerNorm into the QKV / fc1 GEMMs (bf16 default)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
