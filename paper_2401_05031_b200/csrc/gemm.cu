@@ -621,38 +621,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
               for (int j = 0; j < CW / 4; ++j) rr[j] = rp[j];
 #pragma unroll
               for (int j = 0; j < CW / 4; ++j) {
-                v[4 * j] += rr[j].x;
-                v[4 * j + 1] += rr[j].y;
-                v[4 * j + 2] += rr[j].z;
-                v[4 * j + 3] += rr[j].w;
+                const float2 lo = f2_unpack(fadd2(f2_pack(v[4 * j], v[4 * j + 1]), f2_pack(rr[j].x, rr[j].y)));
+                const float2 hi = f2_unpack(fadd2(f2_pack(v[4 * j + 2], v[4 * j + 3]), f2_pack(rr[j].z, rr[j].w)));
+                v[4 * j] = lo.x;
+                v[4 * j + 1] = lo.y;
+                v[4 * j + 2] = hi.x;
+                v[4 * j + 3] = hi.y;
               }
             }
           }
           if constexpr (epi_is_ln(EPI)) {
             const float4* c1p = reinterpret_cast<const float4*>(epi.c1 + n0);
             const float4* c2p = reinterpret_cast<const float4*>(epi.c2 + n0);
+            const uint64_t nmu2 = f2_pack(-ln_mu, -ln_mu), rstd2 = f2_pack(ln_rstd, ln_rstd);
 #pragma unroll
             for (int j = 0; j < CW / 4; ++j) {
               const float4 a1 = __ldg(c1p + j), a2 = __ldg(c2p + j);
-              v[4 * j] = fmaf(ln_rstd, fmaf(-ln_mu, a1.x, v[4 * j]), a2.x);
-              v[4 * j + 1] = fmaf(ln_rstd, fmaf(-ln_mu, a1.y, v[4 * j + 1]), a2.y);
-              v[4 * j + 2] = fmaf(ln_rstd, fmaf(-ln_mu, a1.z, v[4 * j + 2]), a2.z);
-              v[4 * j + 3] = fmaf(ln_rstd, fmaf(-ln_mu, a1.w, v[4 * j + 3]), a2.w);
+              const float2 lo = f2_unpack(ffma2(rstd2, ffma2(nmu2, f2_pack(a1.x, a1.y), f2_pack(v[4 * j], v[4 * j + 1])),
+                                                f2_pack(a2.x, a2.y)));
+              const float2 hi = f2_unpack(ffma2(rstd2, ffma2(nmu2, f2_pack(a1.z, a1.w), f2_pack(v[4 * j + 2], v[4 * j + 3])),
+                                                f2_pack(a2.z, a2.w)));
+              v[4 * j] = lo.x;
+              v[4 * j + 1] = lo.y;
+              v[4 * j + 2] = hi.x;
+              v[4 * j + 3] = hi.y;
             }
           } else {
             const float4* bp = reinterpret_cast<const float4*>(epi.bias + n0);
 #pragma unroll
             for (int j = 0; j < CW / 4; ++j) {
               const float4 b = epi.skip == 3 ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(bp + j);
-              v[4 * j] += b.x;
-              v[4 * j + 1] += b.y;
-              v[4 * j + 2] += b.z;
-              v[4 * j + 3] += b.w;
+              const float2 lo = f2_unpack(fadd2(f2_pack(v[4 * j], v[4 * j + 1]), f2_pack(b.x, b.y)));
+              const float2 hi = f2_unpack(fadd2(f2_pack(v[4 * j + 2], v[4 * j + 3]), f2_pack(b.z, b.w)));
+              v[4 * j] = lo.x;
+              v[4 * j + 1] = lo.y;
+              v[4 * j + 2] = hi.x;
+              v[4 * j + 3] = hi.y;
             }
           }
           if constexpr (epi_is_gelu(EPI)) {
 #pragma unroll
-            for (int j = 0; j < CW; ++j) v[j] = gelu_erf_fast(v[j]);
+            for (int j = 0; j < CW; j += 2) {
+              const float2 gv = f2_unpack(gelu_poly2(f2_pack(v[j], v[j + 1])));
+              v[j] = gv.x;
+              v[j + 1] = gv.y;
+            }
           }
           if constexpr (epi_is_stats(EPI)) {
             // bf16 copy of the stored row chunk (next GEMM's A operand) + row statistics
