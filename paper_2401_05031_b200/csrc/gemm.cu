@@ -671,15 +671,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
             // bf16 copy of the stored row chunk (next GEMM's A operand) + row statistics
             if (row_ok) {
               uint4* xr = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.xh) + orow * N + n0);
+              static_assert(CW % 16 == 0, "32-byte xh stores");
 #pragma unroll
-              for (int j = 0; j < CW / 8; ++j)
-                xr[j] = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
-                                   pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+              for (int j = 0; j < CW / 16; ++j)  // full 32-byte sectors (STG.256)
+                stg256(xr + 2 * j,
+                       make_uint4(pack_bf16(v[16 * j], v[16 * j + 1]), pack_bf16(v[16 * j + 2], v[16 * j + 3]),
+                                  pack_bf16(v[16 * j + 4], v[16 * j + 5]), pack_bf16(v[16 * j + 6], v[16 * j + 7])),
+                       make_uint4(pack_bf16(v[16 * j + 8], v[16 * j + 9]), pack_bf16(v[16 * j + 10], v[16 * j + 11]),
+                                  pack_bf16(v[16 * j + 12], v[16 * j + 13]), pack_bf16(v[16 * j + 14], v[16 * j + 15])));
+              uint64_t s2 = 0ull, q2 = 0ull;  // packed partial sums (two chains)
 #pragma unroll
-              for (int j = 0; j < CW; ++j) {
-                st_s += v[j];
-                st_q = fmaf(v[j], v[j], st_q);
+              for (int j = 0; j < CW; j += 2) {
+                const uint64_t p = f2_pack(v[j], v[j + 1]);
+                s2 = fadd2(s2, p);
+                q2 = ffma2(p, p, q2);
               }
+              const float2 sv = f2_unpack(s2), qv = f2_unpack(q2);
+              st_s += sv.x + sv.y;
+              st_q += qv.x + qv.y;
             }
           }
 #pragma unroll
