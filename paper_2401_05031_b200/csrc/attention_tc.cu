@@ -644,7 +644,7 @@ int attention_tc(const void* qkv, const float* size, int B, int t, int H, int hd
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const float scale_log2 = 1.4426950408889634f / 8.0f;

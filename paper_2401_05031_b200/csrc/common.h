@@ -72,6 +72,9 @@ int set_last_cuda_error(cudaError_t e);
 
 int device_sm_count();
 
+// Programmatic dependent launch on every kernel (TA_PDL=0 disables it: profiling A/B).
+int pdl_enabled();
+
 struct HeadDesc {
   const float* w;  // [classes, D]
   const float* b;  // [classes]

@@ -39,6 +39,15 @@ int device_sm_count() {
   return count;
 }
 
+int pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* v = getenv("TA_PDL");
+    on = (v && v[0] == '0') ? 0 : 1;
+  }
+  return on;
+}
+
 static int check_arch(int device) {
   int major = 0, minor = 0;
   cudaError_t e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
