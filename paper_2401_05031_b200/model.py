@@ -28,7 +28,7 @@ from .core import Batch, us_from_s
 from .errors import ConfigError, ProfileGapError
 from .profiles import ProfileTable
 
-__all__ = ["TransformerModel", "TaskModel", "ServeModel"]
+__all__ = ["TransformerModel", "TaskModel", "ServeModel", "PendingForward"]
 
 _DTYPES = {"bf16": _cuda.DTYPE_BF16, "fp32": _cuda.DTYPE_F32}
 
@@ -181,6 +181,48 @@ class TransformerModel:
         _cuda.check(rc, gamma=gamma)
         return out
 
+    def forward_host_async(self, images: torch.Tensor, task_ids: torch.Tensor, gamma: int,
+                           out: Optional[torch.Tensor] = None) -> "PendingForward":
+        """Pipelined host path: pinned host images -> device (copy stream, one of two staging
+        slots) -> forward on the model's current stream -> logits back into the pinned
+        ``out``; returns at once with a handle (``wait()`` -> logits).  Consecutive calls overlap
+        the next batch's H2D with the current forward, so a stream of host batches runs at the
+        device rate instead of copy + compute + copy in series."""
+        b = images.shape[0]
+        if images.dtype != torch.float32 or images.device.type != "cpu":
+            raise ValueError("images must be fp32 host tensors (pinned for overlap)")
+        if out is None:
+            out = torch.empty(b, self.max_classes, dtype=torch.float32, pin_memory=True)
+        if not hasattr(self, "_copy_stream"):
+            self._copy_stream = torch.cuda.Stream(self.device)
+            self._slots: List[Dict[str, object]] = [{}, {}]
+            self._slot_k = 0
+        slot = self._slots[self._slot_k & 1]
+        self._slot_k += 1
+        shape = tuple(images.shape)
+        if slot.get("shape") != shape:
+            slot.update(shape=shape, img=torch.empty(shape, dtype=torch.float32, device=self.device),
+                        ids=torch.empty(b, dtype=torch.int32, device=self.device),
+                        logits=torch.empty(b, self.max_classes, dtype=torch.float32, device=self.device),
+                        free=None)
+        compute = torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(self._copy_stream):
+            if slot["free"] is not None:  # the forward that last read this slot is done
+                self._copy_stream.wait_event(slot["free"])
+            slot["img"].copy_(images, non_blocking=True)
+            slot["ids"].copy_(task_ids.to(torch.int32), non_blocking=True)
+            h2d = torch.cuda.Event()
+            h2d.record(self._copy_stream)
+        compute.wait_event(h2d)
+        self.forward_raw(slot["img"], slot["ids"], gamma, logits=slot["logits"])
+        free = torch.cuda.Event()
+        free.record(compute)
+        slot["free"] = free
+        out.copy_(slot["logits"], non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(compute)
+        return PendingForward(done, out)
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             torch.cuda.synchronize(self.device)
@@ -192,6 +234,18 @@ class TransformerModel:
             self.close()
         except Exception:
             pass
+
+
+@dataclass
+class PendingForward:
+    """Handle of ``forward_host_async``: ``wait()`` blocks until the logits are on the host."""
+
+    event: object
+    logits: torch.Tensor
+
+    def wait(self) -> torch.Tensor:
+        self.event.synchronize()
+        return self.logits
 
 
 @dataclass
@@ -270,6 +324,15 @@ class ServeModel:
         return self.backbone.forward_raw(inputs.float().contiguous(), ids.to(self.backbone.device), gamma)
 
     __call__ = forward
+
+    def forward_async(self, inputs: torch.Tensor, tasks, gamma: int = 0,
+                      out: Optional[torch.Tensor] = None) -> PendingForward:
+        """Host-batch pipelining over ``TransformerModel.forward_host_async``: returns at once;
+        ``.wait()`` gives the host logits.  Submitting the next batch before waiting overlaps
+        its H2D copy with the current forward."""
+        ids = self.task_ids(tasks)
+        self._check_gamma(ids, gamma)
+        return self.backbone.forward_host_async(inputs.float(), ids, gamma, out=out)
 
     def execute(self, batch: Batch, gamma: int, payloads: Dict[int, torch.Tensor]) -> Tuple[int, List[int]]:
         """Run a planned batch (engine step) and return (latency_us, predictions).

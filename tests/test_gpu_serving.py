@@ -32,3 +32,24 @@ def test_gpu_serving_trace(policy):
         assert set(rep.gamma_counts) == {policy}
     for r in replicas:
         r.backbone.close()
+
+
+def test_forward_async_matches_sync():
+    """ServeModel.forward_async (pipelined H2D / forward / D2H over two staging slots) gives
+    the same logits as the synchronous host path, across gammas and in-flight reuse."""
+    import torch
+
+    gammas = (-4, 0, 4)
+    replicas, index = build_replicas("vit_tiny", ["cuda:0"], DEFAULT_TASKS, gammas)
+    sm = replicas[0]
+    B = 12
+    imgs = [torch.randn(B, 3, 64, 64, generator=torch.Generator().manual_seed(i)).pin_memory() for i in range(6)]
+    tasks = [["CIFAR10", "CIFAR100", "EuroSAT"][i % 3] for i in range(B)]
+    ref = [sm.forward(imgs[i], tasks, gamma=gammas[i % 3]).clone() for i in range(6)]
+    pend = [sm.forward_async(imgs[i], tasks, gamma=gammas[i % 3]) for i in range(6)]
+    for r, p in zip(ref, pend):
+        out = p.wait()
+        fin = torch.isfinite(r)
+        assert torch.equal(fin, torch.isfinite(out))
+        assert torch.equal(r[fin], out[fin])
+    sm.backbone.close()
