@@ -59,6 +59,7 @@ struct GemmEpi {
   const float* c2 = nullptr;        // consumer: [N]
   float inv_dim = 0.f;              // consumer: 1 / D
   int skip = 0;                     // profiling only (TA_GEMM_SKIP_EPILOGUE=1): no epilogue work
+  int direct_store = 0;             // TA_GEMM_STORE=direct: STG.256 rows instead of TMA boxes
 };
 
 __host__ __device__ inline long long epi_out_row(const GemmEpi& e, long long m) {

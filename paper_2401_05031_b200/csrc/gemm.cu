@@ -746,10 +746,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
         };
         // (Interleaved per box.  Reading every box and releasing the accumulator before any
         // staging wait measured slower: the extra live registers cost more than the wait.)
+        // Direct path (TA_GEMM_STORE=direct, profiling A/B): each thread writes its row's
+        // 128-byte box as four 32-byte STG.256 stores instead of the smem box + TMA store.
+        auto direct_store = [&](int c, const uint4 (&w)[8]) {
+          if (!row_ok || epi.skip == 2) return;
+          const int n0 = n_blk * BN + col0 + c * CW;
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<OutT*>(epi.out) + m * N + n0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) stg256(dst + 2 * j, w[2 * j], w[2 * j + 1]);
+        };
 #pragma unroll 1
         for (int c = 0; c < NCH; ++c) {
           uint4 w[8];
-          if (compute(c, w)) stage_store(c, w);
+          if (compute(c, w)) {
+            if (!kRemap && epi.direct_store)
+              direct_store(c, w);
+            else
+              stage_store(c, w);
+          }
         }
         if constexpr (epi_is_stats(EPI)) {
           static_assert(BN / kSplit == 128, "one stats slot per warp and tile");
@@ -1093,8 +1107,13 @@ int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, b
     const char* v = getenv("TA_GEMM_SKIP_EPILOGUE");
     return v ? atoi(v) : 0;
   }();
+  static const int direct = [] {
+    const char* v = getenv("TA_GEMM_STORE");
+    return (v && v[0] == 'd') ? 1 : 0;
+  }();
   GemmEpi epi = epi_in;
   epi.skip = skip_epi;
+  epi.direct_store = direct;
   if (M <= 0) return TA_OK;
   if (K % kBK != 0 || N % 128 != 0) return TA_ERR_SHAPE;
   if ((epi_is_resid(epi_kind) || epi_is_patch(epi_kind)) && out_bf16) return TA_ERR_INVALID;

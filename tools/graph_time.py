@@ -27,3 +27,11 @@ for g in gammas:
     for _ in range(20): graphs[g].replay()
     e1.record(); e1.synchronize()
     print(f"TA_PDL={os.environ.get('TA_PDL', '1')} gamma {g:4d}: {e0.elapsed_time(e1) / 20:.3f} ms")
+# eager launches of the same forwards for comparison
+for g in gammas:
+    for _ in range(3): bb.forward_raw(imgs, ids, g)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20): bb.forward_raw(imgs, ids, g)
+    e1.record(); e1.synchronize()
+    print(f"eager gamma {g:4d}: {e0.elapsed_time(e1) / 20:.3f} ms")
