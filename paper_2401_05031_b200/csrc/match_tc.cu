@@ -53,9 +53,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   const int nkc = cp / 32;                   // 32-float K chunks (128-byte swizzle rows)
   const int tile_bytes = nkc * kRows * 128;  // one part
   float* node_max = reinterpret_cast<float*>(smem + 4 * tile_bytes);
-  int* node_idx = reinterpret_cast<int*>(node_max + kRows);
-  int* rank = node_idx + kRows;
-  uint64_t* bar_mma = reinterpret_cast<uint64_t*>(rank + kRows);
+  int* node_idx = reinterpret_cast<int*>(node_max + 2 * kRows);
+  int* rank = node_idx + 2 * kRows;
+  uint64_t* bar_mma = reinterpret_cast<uint64_t*>(rank + 2 * kRows);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_mma + 1);
   const int tid = threadIdx.x;
   const uint32_t warp = warp_id(), lane = lane_id();
@@ -71,81 +71,76 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 
   // ---- phase 1: metric rows -> normalised, split, swizzled smem tiles
   const long long D = static_cast<long long>(heads) * c;
+  // Smem row of token tok: B = odd tokens at row tok / 2; A = even tokens without the class
+  // token (its S row is -inf by definition) at row tok / 2 - 1, so na <= 129 (t <= 257) fits
+  // the M = 128 MMA.
+  auto smem_row = [](int tok) { return (tok & 1) ? (tok >> 1) : (tok >> 1) - 1; };
   if constexpr (sizeof(QT) == 2) {
     if (metric == nullptr) {
-      // bf16 k: a warp covers a row pair (lanes 0..15 the even token -> set A, 16..31 the odd
-      // one -> set B), 4 columns (8 bytes) per lane and head; two pairs per iteration with
-      // every head's load issued before the head-order sums, so ~6 KB per warp are in flight.
-      const int sub = static_cast<int>(lane) >> 4;
-      const int cl = (static_cast<int>(lane) & 15) * 4;
-      const int n_pairs = (t + 1) / 2;
-      for (int p0 = static_cast<int>(warp); p0 < n_pairs; p0 += 2 * (kFusedThreads / 32)) {
-        uint2 raw[2][kU][16];
+      // bf16 k: rows in lane segments of kSeg lanes, 8 columns (16 bytes) per lane and head
+      // (c = 64: 8 lanes, 4 rows per warp; c = 80: 10 of 16 lanes, 2 rows per warp); kPP row
+      // groups per iteration with every head's load issued before the head-order sums.
+      constexpr int kSeg = kU == 1 ? 8 : 16;
+      constexpr int kRowsPerWarp = 32 / kSeg;
+      constexpr int kPP = 1;  // (2 row groups in flight spill at 16 heads x 16 bytes)
+      const int seg = static_cast<int>(lane) / kSeg, sl = static_cast<int>(lane) % kSeg;
+      const int j = 8 * sl;  // first column of this lane
+      constexpr int kStep = kRowsPerWarp * (kFusedThreads / 32);
+      for (int t0 = static_cast<int>(warp) * kRowsPerWarp; t0 < t; t0 += kPP * kStep) {
+        uint4 raw[kPP][16];
 #pragma unroll
-        for (int pp = 0; pp < 2; ++pp) {
-          const int tok = 2 * (p0 + pp * (kFusedThreads / 32)) + sub;
+        for (int pp = 0; pp < kPP; ++pp) {
+          const int tok = t0 + pp * kStep + seg;
+          if (tok < t && j < c) {
+            const QT* kr = qkv + (static_cast<long long>(b) * t + tok) * 3 * D + D + j;
 #pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int j = cl + 64 * u;
-            if (tok < t && j < c) {
-              const QT* kr = qkv + (static_cast<long long>(b) * t + tok) * 3 * D + D + j;
-#pragma unroll
-              for (int hh = 0; hh < 16; ++hh)
-                if (hh < heads) raw[pp][u][hh] = __ldg(reinterpret_cast<const uint2*>(kr + hh * c));
-            }
+            for (int hh = 0; hh < 16; ++hh)
+              if (hh < heads) raw[pp][hh] = __ldg(reinterpret_cast<const uint4*>(kr + hh * c));
           }
         }
 #pragma unroll
-        for (int pp = 0; pp < 2; ++pp) {
-          const int tok = 2 * (p0 + pp * (kFusedThreads / 32)) + sub;
-          float v[kU][4];
-          float ss = 0.f;
+        for (int pp = 0; pp < kPP; ++pp) {
+          const int tok = t0 + pp * kStep + seg;
+          float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          if (tok < t && j < c) {
 #pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int j = cl + 64 * u;
-            float a[4] = {0.f, 0.f, 0.f, 0.f};
-            if (tok < t && j < c) {
-#pragma unroll
-              for (int hh = 0; hh < 16; ++hh) {
-                if (hh < heads) {
-                  const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw[pp][u][hh].x));
-                  const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw[pp][u][hh].y));
-                  a[0] += lo.x;
-                  a[1] += lo.y;
-                  a[2] += hi.x;
-                  a[3] += hi.y;
-                }
-              }
-            }
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              v[u][e] = a[e] / heads;
-              ss += v[u][e] * v[u][e];
-            }
-          }
-          // norm over the 16 lanes of this row
-#pragma unroll
-          for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-          const float nrm = sqrtf(ss);
-          if (tok < t) {
-            const int ri = tok >> 1;
-            const uint32_t row_hi = s0 + (sub * 2) * tile_bytes + ri * 128;
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {
-              const int j = cl + 64 * u;
-              if (j < cp) {
-                float hv[4], lv[4];
+            for (int hh = 0; hh < 16; ++hh) {
+              if (hh < heads) {
+                const uint32_t w4[4] = {raw[pp][hh].x, raw[pp][hh].y, raw[pp][hh].z, raw[pp][hh].w};
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                  const float x = j + e < c ? v[u][e] / nrm : 0.f;
-                  hv[e] = tf32_trunc(x);
-                  lv[e] = tf32_trunc(x - hv[e]);
+                  const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
+                  a[2 * e] += f.x;
+                  a[2 * e + 1] += f.y;
                 }
-                const int kc = j >> 5, jj = j & 31;
-                const uint32_t off = kc * kRows * 128 + (((jj >> 2) ^ (ri & 7)) << 4);
-                sts_f4(row_hi + off, make_float4(hv[0], hv[1], hv[2], hv[3]));
-                sts_f4(row_hi + tile_bytes + off, make_float4(lv[0], lv[1], lv[2], lv[3]));
               }
+            }
+          }
+          float ss = 0.f;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            a[e] /= heads;
+            ss += a[e] * a[e];
+          }
+#pragma unroll
+          for (int o = kSeg / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+          const float nrm = sqrtf(ss);
+          if (tok < t && tok > 0 && j < cp) {
+            const int ri = smem_row(tok);
+            const uint32_t row_hi = s0 + ((tok & 1) * 2) * tile_bytes + ri * 128;
+            float hv[8], lv[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float x = j + e < c ? a[e] / nrm : 0.f;
+              hv[e] = tf32_trunc(x);
+              lv[e] = tf32_trunc(x - hv[e]);
+            }
+            const int kc = j >> 5, jj = j & 31;
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const uint32_t off = kc * kRows * 128 + ((((jj >> 2) + h2) ^ (ri & 7)) << 4);
+              sts_f4(row_hi + off, make_float4(hv[4 * h2], hv[4 * h2 + 1], hv[4 * h2 + 2], hv[4 * h2 + 3]));
+              sts_f4(row_hi + tile_bytes + off, make_float4(lv[4 * h2], lv[4 * h2 + 1], lv[4 * h2 + 2], lv[4 * h2 + 3]));
             }
           }
         }
@@ -191,7 +186,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         ss += v[u][0] * v[u][0] + v[u][1] * v[u][1];
       }
       const float nrm = sqrtf(warp_sum(ss));
-      const int set = tok & 1, ri = tok >> 1;
+      if (tok == 0) continue;  // the class token never enters the MMA (its S row is -inf)
+      const int set = tok & 1, ri = smem_row(tok);
       const uint32_t row_hi = s0 + (set * 2) * tile_bytes + ri * 128;
   #pragma unroll
       for (int u = 0; u < 2; ++u) {
@@ -237,7 +233,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     __syncwarp();
     mbar_wait(bar_mma, 0);
     tc_fence_after();
-    // ---- phase 3: row max / argmax of S[i, 0..nb) from TMEM (thread i = lane i)
+    // ---- phase 3: row max / argmax of S[i, 0..nb) from TMEM: thread i = TMEM lane i = A
+    // row i + 1 (the class token, A row 0, is not in the MMA and gets -inf below)
     float best = -INFINITY;
     int best_j = 0;
     const uint32_t la = tmem + ((warp * 32u) << 16);
@@ -245,19 +242,23 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       uint32_t v[32];
       tmem_ld_32x32b_x32(la + c0, v);
       tmem_ld_wait();
-      if (i > 0) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float sv = __uint_as_float(v[j]);
-          if (c0 + j < nb && sv > best) {  // ascending j, strict >: lowest column on ties
-            best = sv;
-            best_j = c0 + j;
-          }
+      for (int j = 0; j < 32; ++j) {
+        const float sv = __uint_as_float(v[j]);
+        if (c0 + j < nb && sv > best) {  // ascending j, strict >: lowest column on ties
+          best = sv;
+          best_j = c0 + j;
         }
       }
     }
-    node_max[i] = i < na ? best : -INFINITY;
-    node_idx[i] = best_j;
+    if (i + 1 < na) {
+      node_max[i + 1] = best;
+      node_idx[i + 1] = best_j;
+    }
+    if (i == 0) {
+      node_max[0] = -INFINITY;
+      node_idx[0] = 0;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -313,15 +314,15 @@ cudaError_t launch_pdl(void (*kern)(Args...), dim3 grid, dim3 block, size_t smem
 // tensor-core path in match() (tome.cu), so a token allocation is kept in the workspace.
 size_t match_tc_scratch_bytes(int, int) { return 256; }
 
-// Returns TA_ERR_SHAPE outside the kernel's envelope (t > 256, c > 96 or > 16 heads).
+// Returns TA_ERR_SHAPE outside the kernel's envelope (t > 257, c > 96 or > 16 heads).
 int match_tc(const float* metric, const void* qkv, int qkv_dtype, int B, int t, int heads, int c,
              int r, int32_t* src, int32_t* dst, int32_t* unm, float* scratch, cudaStream_t s) {
   (void)scratch;
   const int na = (t + 1) / 2;
   if (r <= 0 || r > na - 1 || t < 3) return TA_ERR_INVALID;
-  if (t > 2 * kRows || c > 96 || (c & 1) || heads > 16) return TA_ERR_SHAPE;
+  if (t > 2 * kRows + 1 || c > 96 || c % 8 || heads > 16) return TA_ERR_SHAPE;
   const int cp = (c + 31) / 32 * 32;
-  const size_t smem = 4 * (cp / 32) * kRows * 128 + 3 * kRows * 4 + 64 + 1024;
+  const size_t smem = 4 * (cp / 32) * kRows * 128 + 3 * 2 * kRows * 4 + 64 + 1024;
   static bool attr_set = false;
   cudaError_t e;
   if (!attr_set) {

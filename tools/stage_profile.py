@@ -5,12 +5,13 @@ import torch
 from tests import helpers
 g = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 fold = bool(int(sys.argv[2])) if len(sys.argv) > 2 else False
-cfg, params = helpers.backbone("vit_b16")
+MODEL = os.environ.get("MODEL", "vit_b16"); BATCH = int(os.environ.get("BATCH", "256"))
+cfg, params = helpers.backbone(MODEL)
 tasks = helpers.task_params(cfg, (100,), [g] if g > 0 else [])
 sm = helpers.serve_model(cfg, params, tasks, dtype="bf16", fold_ln=fold)
 bb = sm.backbone
-imgs = torch.randn(256, 3, 224, 224, device="cuda")
-ids = torch.zeros(256, dtype=torch.int32, device="cuda")
+imgs = torch.randn(BATCH, 3, cfg.img, cfg.img, device="cuda")
+ids = torch.zeros(BATCH, dtype=torch.int32, device="cuda")
 for _ in range(3): bb.forward_raw(imgs, ids, g)
 torch.cuda.synchronize()
 os.environ["TA_PROFILE_STAGES"] = "1"
