@@ -175,7 +175,7 @@ def run_ours(args):
     torch.cuda.set_device(dev)
 
     cfg, params = helpers.backbone(args.model)
-    gammas = GAMMAS
+    gammas = tuple(int(g) for g in args.gammas.split(",")) if args.gammas else GAMMAS
     tasks = helpers.task_params(cfg, (100,), [g for g in gammas if g > 0])
     sm = helpers.serve_model(cfg, params, tasks, dtype="bf16", fold_ln=bool(args.fold_ln))
     bb = sm.backbone
@@ -275,7 +275,8 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(total_ms / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"{args.model} batch {B} per gamma, sweep gamma in {list(gammas)} (configs[1]); one step = the sweep",
+            "config": {"workload": f"{args.model} batch {B} per gamma, sweep gamma in {list(gammas)}"
+                                   f"{' (configs[1])' if args.model == 'vit_b16' and gammas == GAMMAS and B == 256 else ''}; one step = the sweep",
                        "model": args.model, "global_batch": B * len(gammas) * world, "seq_len": cfg.n_tokens,
                        "parallelism": f"replicas x{world} (no collectives)", "prompt_mode": "accumulate",
                        "l2": "flushed (512 MiB write) before every step; inputs 154 MB per gamma > L2",
@@ -365,6 +366,7 @@ def main():
     ap.add_argument("--cpu-batch", type=int, default=8)
     ap.add_argument("--ref-batch", type=int, default=4)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--gammas", default="", help="comma-separated gamma sweep (default configs[1]: -16,-8,0,8,16)")
     ap.add_argument("--fold-ln", type=int, default=1, help="fold LayerNorm into the QKV / fc1 GEMMs (bf16 default)")
     args = ap.parse_args()
     if args.impl == "reference":
