@@ -298,6 +298,8 @@ __global__ void __launch_bounds__(128)
 // kernel for t <= 64 (one 64-row query tile: 24.7 vs 37.4 us at t = 53), the whole-row tcgen05
 // kernel (attention_tc.cu) for 64 < t <= 512 (117 vs 213 / 239 us at t = 197), the chunk-
 // pipelined tcgen05 kernel (attention_fa.cu) beyond (1420 vs 1771 us at t = 581, H = 16).
+// head_dim 80 (ViT-H/14): the whole-row tcgen05 kernel with a 16-column SW32 tail for
+// 64 < t <= 512 (1066 vs 1391 us at t = 257, B = 512, H = 16), mma.sync otherwise.
 // TA_ATTENTION_BACKEND=tc / fa / mma forces one kernel (the parity tests cover all three).
 static int attention_backend() {
   static int mode = -1;

@@ -1,5 +1,10 @@
 // Proportional attention on the 5th-gen tensor cores (north_star 3):
-//   o = softmax(q k^T / sqrt(hd) + log size_j) v        per (image, head), hd = 64, t <= 512
+//   o = softmax(q k^T / sqrt(hd) + log size_j) v        per (image, head), hd = 64 / 80, t <= 512
+//
+// head_dim 80 (ViT-H/14): every Q / K / V row is a 64-column SW128 part plus a 16-column SW32
+// tail (its own TMA map); S = Q K^T takes the tail as a fifth K = 16 step, O += P V a second
+// N = 16 MMA into O[64, 80); O[0, 80) then overlaps S block 1 as well, so a tile's first PV
+// waits until block 1's P is written; the tail columns of O leave by one STG.256 per row.
 //
 // Persistent, warp-specialised, one CTA per SM looping over work items (image, head); each
 // item walks its 128-query tiles with K / V fetched from HBM once per item.
@@ -46,6 +51,11 @@ constexpr int kMaxTPad = 512;
 constexpr int kThreads = 320;
 
 struct AttnTcLayout {
+  int hd;       // 64, or 80 = a 64-column SW128 part + a 16-column SW32 tail
+  int tail;     // hd - 64
+  uint32_t q_bytes;   // Q tile: 128 x 64 main (16 KB) + 128 x tail (SW32)
+  uint32_t tail_blk;  // bytes of one 64-key block's tail columns (64 x tail x 2)
+  uint32_t kt_off, vt_off;  // K / V tail regions inside a K/V slot
   int t_pad;    // round_up(t, 64)
   int t_mma;    // round_up(t, 16): S MMA N (keys past it are never read)
   int nch_last; // 8-key chunks of the last 64-key block holding keys < t
@@ -59,8 +69,12 @@ struct AttnTcLayout {
   uint32_t kv_off, p_off, bias_off, red_off, bar_off, smem_bytes;
 };
 
-AttnTcLayout attn_layout(int t) {
+AttnTcLayout attn_layout(int t, int hd) {
   AttnTcLayout L{};
+  L.hd = hd;
+  L.tail = hd - kHd;
+  L.q_bytes = kQBytes + kQTile * L.tail * 2;
+  L.tail_blk = kKeyBlk * L.tail * 2;
   L.t_pad = (t + kKeyBlk - 1) / kKeyBlk * kKeyBlk;
   L.n_kb = L.t_pad / kKeyBlk;
   L.t_mma = (t + 15) / 16 * 16;
@@ -77,8 +91,13 @@ AttnTcLayout attn_layout(int t) {
   L.rowsplit = L.t_pad <= 256;
   if (const char* e = getenv("TA_ATTN_SPLIT"))  // profiling override: "row" / "key"
     L.rowsplit = L.t_pad <= 256 && e[0] != 'k';
-  L.kv_bytes = 2u * L.n_kb * kBlkBytes;
-  uint32_t off = kQBytes;  // Q: one slot (Q(n+1) is only needed after S(n) has long completed)
+  // K/V slot: [K main blocks][V main blocks][K tails][V tails]
+  L.kt_off = 2u * L.n_kb * kBlkBytes;
+  L.vt_off = L.kt_off + L.n_kb * L.tail_blk;
+  L.kv_bytes = L.vt_off + L.n_kb * L.tail_blk;
+  // hd = 80 at t_pad = 256: two K/V slots would not fit beside Q and the P ring
+  if (L.n_kv == 2 && L.q_bytes + 2 * L.kv_bytes + 4 * kPBytes + 8192 > 227u * 1024) L.n_kv = 1;
+  uint32_t off = (L.q_bytes + 1023) / 1024 * 1024;  // Q: one slot (Q(n+1) is only needed after S(n))
   L.kv_off = off;
   off += L.n_kv * L.kv_bytes;
   L.p_off = off;
@@ -111,9 +130,10 @@ __device__ unsigned int g_trace_tag[16384];
 #define TRACE_DECL do {} while (0)
 #endif
 
-template <bool kHasSize>
+template <bool kHasSize, int kHD>
 __global__ void __launch_bounds__(kThreads, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo,
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmt,
+                   const __grid_constant__ CUtensorMap tmo,
                    const float* __restrict__ size, int t,
                    int H, int n_items, __nv_bfloat16* __restrict__ out, float scale_log2,
                    AttnTcLayout L) {
@@ -121,7 +141,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  const int D = H * kHd;
+  constexpr int kTail = kHD - kHd;  // 16-column SW32 tail of a head_dim = 80 row (0 for 64)
+  const int D = H * kHD;
   uint8_t* sQ = smem;
   uint8_t* sKV = smem + L.kv_off;
   uint8_t* sP = smem + L.p_off;
@@ -200,17 +221,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         TRACE(1);
         mbar_arrive_expect_tx(&kv_full[kvs], L.kv_bytes);
         for (int kb = 0; kb < L.n_kb; ++kb) {
-          tma_load_2d(&tm, &kv_full[kvs], sK + kb * kBlkBytes, D + h * kHd, row_base + kb * kKeyBlk);
-          tma_load_2d(&tm, &kv_full[kvs], sV + kb * kBlkBytes, 2 * D + h * kHd, row_base + kb * kKeyBlk);
+          tma_load_2d(&tm, &kv_full[kvs], sK + kb * kBlkBytes, D + h * kHD, row_base + kb * kKeyBlk);
+          tma_load_2d(&tm, &kv_full[kvs], sV + kb * kBlkBytes, 2 * D + h * kHD, row_base + kb * kKeyBlk);
+          if constexpr (kTail > 0) {
+            tma_load_2d(&tmt, &kv_full[kvs], sK + L.kt_off + kb * L.tail_blk, D + h * kHD + kHd,
+                        row_base + kb * kKeyBlk);
+            tma_load_2d(&tmt, &kv_full[kvs], sK + L.vt_off + kb * L.tail_blk, 2 * D + h * kHD + kHd,
+                        row_base + kb * kKeyBlk);
+          }
         }
         for (int qt = 0; qt < L.n_qt; ++qt, ++qcnt) {
           mbar_wait(&q_free[0], (qcnt & 1) ^ 1);
 #ifdef TA_ATTN_EXP_QONCE  // profiling only: wrong results (Q of the first tile reused)
           if (qcnt > 0) { mbar_arrive(&q_full[0]); continue; }
 #endif
-          mbar_arrive_expect_tx(&q_full[0], kQBytes);
-          tma_load_2d(&tm, &q_full[0], sQ, h * kHd, row_base + qt * kQTile);
-          tma_load_2d(&tm, &q_full[0], sQ + kBlkBytes, h * kHd, row_base + qt * kQTile + 64);
+          mbar_arrive_expect_tx(&q_full[0], L.q_bytes);
+          tma_load_2d(&tm, &q_full[0], sQ, h * kHD, row_base + qt * kQTile);
+          tma_load_2d(&tm, &q_full[0], sQ + kBlkBytes, h * kHD, row_base + qt * kQTile + 64);
+          if constexpr (kTail > 0) {
+            tma_load_2d(&tmt, &q_full[0], sQ + kQBytes, h * kHD + kHd, row_base + qt * kQTile);
+            tma_load_2d(&tmt, &q_full[0], sQ + kQBytes + 64 * kTail * 2, h * kHD + kHd,
+                        row_base + qt * kQTile + 64);
+          }
           TRACE(2);
         }
       }
@@ -219,30 +251,43 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_pv = idesc_bf16(kQTile, kHd, /*b_mn_major=*/true);
+      constexpr uint32_t idesc_pv_t = idesc_bf16(kQTile, kTail > 0 ? kTail : 16, /*b_mn_major=*/true);
+      // O += P_blk V_blk for one 64-key block: N = 64 from the SW128 V part into O[0, 64) and,
+      // for head_dim 80, N = 16 from the SW32 tail into O[64, 80).
+      auto pv_block = [&](uint32_t o_tmem, uint64_t pdesc, const uint8_t* sKVslot, int kb, int nkc) {
+        const uint32_t vbase = smem_u32(sKVslot + L.n_kb * kBlkBytes + kb * kBlkBytes);
+        const uint32_t vtbase = smem_u32(sKVslot + L.vt_off + kb * L.tail_blk);
+#pragma unroll
+        for (int kc = 0; kc < kKeyBlk / 16; ++kc) {
+          if (kc >= nkc) break;
+          // V rows (keys) are the K dimension: 16 keys = two 8-row groups = 2048 B.
+          const uint64_t vdesc = umma_desc_sw128_mn(vbase + kc * 2048, 8192, 1024);
+          umma_f16(o_tmem, pdesc + 2 * kc, vdesc, idesc_pv, (kb | kc) != 0);
+          if constexpr (kTail > 0) {
+            const uint64_t vtdesc = umma_desc_sw32_mn(vtbase + kc * 512, 512, 256);
+            umma_f16(o_tmem + kHd, pdesc + 2 * kc, vtdesc, idesc_pv_t, (kb | kc) != 0);
+          }
+        }
+      };
       uint32_t p_use[2] = {0, 0};  // per softmax group; stage = 2 g + (use & 1)
       // pending PV tile (issued after the next tile's S so softmax never waits)
       int pend_slot = -1, pend_kvs = 0;
       bool pend_last = false;
       auto issue_pv = [&](int sslot, int kvs, bool last_of_item) {
-        const uint8_t* sV = sKV + kvs * L.kv_bytes + L.n_kb * kBlkBytes;
+        const uint8_t* sKVslot = sKV + kvs * L.kv_bytes;
         const uint32_t o_tmem = tmem + sslot * 256;
         for (int kb = 0; kb < L.n_kb; ++kb) {
           const int grp = kb & 1;
           const uint32_t u = p_use[grp]++;
           const int ps = 2 * grp + (u & 1);
           mbar_wait(&p_full[ps], (u >> 1) & 1);
+          if (kTail > 0 && kb == 0 && L.n_kb > 1)  // O[0, 80) overlaps S block 1: wait for its P
+            mbar_wait(&p_full[2 + (p_use[1] & 1)], (p_use[1] >> 1) & 1);
           TRACE(5);
           tc_fence_after();
           const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
-          const uint32_t vbase = smem_u32(sV + kb * kBlkBytes);
           const int nkc = kb == L.n_kb - 1 ? L.nkc_last : kKeyBlk / 16;
-#pragma unroll
-          for (int kc = 0; kc < kKeyBlk / 16; ++kc) {
-            if (kc >= nkc) break;
-            // V rows (keys) are the K dimension: 16 keys = two 8-row groups = 2048 B.
-            const uint64_t vdesc = umma_desc_sw128_mn(vbase + kc * 2048, 8192, 1024);
-            umma_f16(o_tmem, pdesc + 2 * kc, vdesc, idesc_pv, (kb | kc) != 0);
-          }
+          pv_block(o_tmem, pdesc, sKVslot, kb, nkc);
           umma_commit(&p_free[ps]);
         }
         umma_commit(&o_full[sslot]);
@@ -281,6 +326,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int k = 0; k < kHd / 16; ++k)
                 umma_f16(tmem + slot * 256, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0);
+              if constexpr (kTail > 0)  // head_dim 80: the 16-column tail as a fifth K step
+                umma_f16(tmem + slot * 256, umma_desc_sw32(smem_u32(sQ + kQBytes)),
+                         umma_desc_sw32(smem_u32(sK + L.kt_off)), idesc_s, 1);
               umma_commit(&s_full[slot]);
               umma_commit(&q_free[0]);
               TRACE(4);
@@ -297,20 +345,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t u = p_use[grp];
             const int ps = 2 * grp + (u & 1);
             if (!mbar_test(&p_full[ps], (u >> 1) & 1)) continue;
+            // head_dim 80: O[0, 80) overlaps S block 1, so block 0's PV waits for block 1's P
+            if (kTail > 0 && pkb[grp] == 0 && L.n_kb > 1 &&
+                !mbar_test(&p_full[2 * grp + ((u + 1) & 1)], ((u + 1) >> 1) & 1))
+              continue;
             TRACE(8 + 16 * grp);
             ++p_use[grp];
             tc_fence_after();
             const int kvs = ring_slot(p_it[grp], L.n_kv);
-            const uint8_t* sV = sKV + kvs * L.kv_bytes + L.n_kb * kBlkBytes;
             const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
-            const uint32_t vbase = smem_u32(sV + pkb[grp] * kBlkBytes);
             const int nkc = pkb[grp] == L.n_kb - 1 ? L.nkc_last : kKeyBlk / 16;
-#pragma unroll
-            for (int kc = 0; kc < kKeyBlk / 16; ++kc) {
-              if (kc >= nkc) break;
-              const uint64_t vdesc = umma_desc_sw128_mn(vbase + kc * 2048, 8192, 1024);
-              umma_f16(tmem + grp * 256, pdesc + 2 * kc, vdesc, idesc_pv, (pkb[grp] | kc) != 0);
-            }
+            pv_block(tmem + grp * 256, pdesc, sKV + kvs * L.kv_bytes, pkb[grp], nkc);
             umma_commit(&p_free[ps]);
             TRACE(5 + 16 * grp);
             if (++pkb[grp] == L.n_kb) {
@@ -356,6 +401,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int k = 0; k < kHd / 16; ++k)
               umma_f16(tmem + ss * 256 + n0, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0);
+            if constexpr (kTail > 0)
+              umma_f16(tmem + ss * 256 + n0, umma_desc_sw32(smem_u32(sQ + kQBytes)),
+                       umma_desc_sw32(smem_u32(sK + L.kt_off + n0 * kTail * 2)), idesc_s, 1);
           }
           umma_commit(&s_full[ss]);
           TRACE(4);
@@ -450,18 +498,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       return rcp_approx(lds_f32(s_red + (256 + i) * 4) + lds_f32(s_red + (384 + i) * 4));
     };
 
+    // head_dim 80: this thread's row's last 16 columns (32 bytes, one STG.256) of O / sum
+    auto store_o_tail = [&](const uint32_t (&ot)[16], float inv, int b, int q, int h) {
+      if (q >= t) return;
+      uint32_t w[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        w[e] = pack_bf16(__uint_as_float(ot[2 * e]) * inv, __uint_as_float(ot[2 * e + 1]) * inv);
+      stg256(out + (static_cast<long long>(b) * t + q) * D + h * kHD + kHd, make_uint4(w[0], w[1], w[2], w[3]),
+             make_uint4(w[4], w[5], w[6], w[7]));
+    };
     auto epilogue = [&](uint32_t tcnt, int b, int h, int qt, float inv) {
       const int ss = ring_slot(tcnt, L.n_s);
       mbar_wait(&o_full[ss], ring_use(tcnt, L.n_s) & 1);
       TRACE(17);
       tc_fence_after();
-      uint32_t o[32];
+      uint32_t o[32], ot[16];
       tmem_ld_32x32b_x32(lane_base + ss * 256 + g * 32, o);
+      if (kTail > 0 && g == 1) tmem_ld_32x32b_x16(lane_base + ss * 256 + kHd, ot);
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&s_free[ss]);
       const int q0 = qt * kQTile + (warp & 3) * 32;
-      if (q0 < t) store_o_slab(&tmo, o, inv, s_slab, lane, h * kHd + g * 32, q0, b);
+      if (q0 < t) store_o_slab(&tmo, o, inv, s_slab, lane, h * kHD + g * 32, q0, b);
+      if (kTail > 0 && g == 1) store_o_tail(ot, inv, b, q0 + static_cast<int>(lane), h);
       TRACE(18);
     };
 
@@ -529,16 +589,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&o_full[g], k & 1);
           TRACE(17);
           tc_fence_after();
-          uint32_t o0[32], o1[32];
+          uint32_t o0[32], o1[32], ot[16];
           tmem_ld_32x32b_x32(la, o0);
           tmem_ld_32x32b_x32(la + 32, o1);
+          if constexpr (kTail > 0) tmem_ld_32x32b_x16(la + kHd, ot);
           tmem_ld_wait();
           tc_fence_before();
           mbar_arrive(&s_free[g]);
           const int q0 = qt * kQTile + (warp & 3) * 32;
           if (q0 < t) {
-            store_o_slab(&tmo, o0, inv, s_slab, lane, h * kHd, q0, b);
-            store_o_slab(&tmo, o1, inv, s_slab + 2048, lane, h * kHd + 32, q0, b);
+            store_o_slab(&tmo, o0, inv, s_slab, lane, h * kHD, q0, b);
+            store_o_slab(&tmo, o1, inv, s_slab + 2048, lane, h * kHD + 32, q0, b);
+            if constexpr (kTail > 0) store_o_tail(ot, inv, b, q0 + static_cast<int>(lane), h);
           }
           TRACE(18);
           ++k;
@@ -614,28 +676,43 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-// Returns TA_ERR_SHAPE when the shape is outside the tcgen05 kernel's envelope
-// (hd != 64 or t > 512); the caller then uses the mma.sync kernel.
-int attention_tc(const void* qkv, const float* size, int B, int t, int H, int hd, void* out,
-                 cudaStream_t s) {
-  if (hd != kHd || t <= 0 || t > kMaxTPad) return TA_ERR_SHAPE;
-  const AttnTcLayout L = attn_layout(t);
-  CUtensorMap tm;
-  int rc = make_tmap_bf16_2d(&tm, qkv, static_cast<uint64_t>(B) * t, 3ull * H * hd, 64);
-  if (rc) return rc;
-  CUtensorMap tmo;
-  rc = make_tmap_attn_out(&tmo, out, B, t, static_cast<uint64_t>(H) * hd);
-  if (rc) return rc;
+int make_tmap_bf16_2d_sw(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                         uint32_t box_cols, uint32_t box_rows, int swizzle_bytes);
+
+template <bool kHasSize, int kHD>
+static cudaError_t launch_attn_tc(const cudaLaunchConfig_t& cfg, const CUtensorMap& tm,
+                                  const CUtensorMap& tmt, const CUtensorMap& tmo, const float* size,
+                                  int t, int H, int n_items, __nv_bfloat16* o, float scale_log2,
+                                  const AttnTcLayout& L) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(attn_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               227 * 1024);
-    if (e != cudaSuccess) return set_last_cuda_error(e);
+    const cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<kHasSize, kHD>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  return cudaLaunchKernelEx(&cfg, attn_tc_kernel<kHasSize, kHD>, tm, tmt, tmo, size, t, H, n_items, o,
+                            scale_log2, L);
+}
+
+// Returns TA_ERR_SHAPE when the shape is outside the tcgen05 kernel's envelope
+// (hd not 64 / 80 or t > 512); the caller then uses another kernel.
+int attention_tc(const void* qkv, const float* size, int B, int t, int H, int hd, void* out,
+                 cudaStream_t s) {
+  if ((hd != 64 && hd != 80) || t <= 0 || t > kMaxTPad) return TA_ERR_SHAPE;
+  const AttnTcLayout L = attn_layout(t, hd);
+  if (L.smem_bytes > 227u * 1024) return TA_ERR_SHAPE;
+  const uint64_t rows = static_cast<uint64_t>(B) * t, cols = 3ull * H * hd;
+  CUtensorMap tm, tmt, tmo;
+  int rc = make_tmap_bf16_2d(&tm, qkv, rows, cols, 64);
+  if (rc) return rc;
+  tmt = tm;
+  if (hd == 80) {  // the 16-column tail of each 80-column head: 32-byte rows, SW32
+    rc = make_tmap_bf16_2d_sw(&tmt, qkv, rows, cols, 16, 64, 32);
+    if (rc) return rc;
+  }
+  rc = make_tmap_attn_out(&tmo, out, B, t, static_cast<uint64_t>(H) * hd);
+  if (rc) return rc;
   const int n_items = B * H;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_items < device_sm_count() ? n_items : device_sm_count());
@@ -647,11 +724,15 @@ int attention_tc(const void* qkv, const float* size, int B, int t, int H, int hd
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const float scale_log2 = 1.4426950408889634f / 8.0f;
+  const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(hd));
   auto* o = static_cast<__nv_bfloat16*>(out);
-  cudaError_t e = size != nullptr
-                      ? cudaLaunchKernelEx(&cfg, attn_tc_kernel<true>, tm, tmo, size, t, H, n_items, o, scale_log2, L)
-                      : cudaLaunchKernelEx(&cfg, attn_tc_kernel<false>, tm, tmo, size, t, H, n_items, o, scale_log2, L);
+  cudaError_t e;
+  if (hd == 64)
+    e = size != nullptr ? launch_attn_tc<true, 64>(cfg, tm, tmt, tmo, size, t, H, n_items, o, scale_log2, L)
+                        : launch_attn_tc<false, 64>(cfg, tm, tmt, tmo, size, t, H, n_items, o, scale_log2, L);
+  else
+    e = size != nullptr ? launch_attn_tc<true, 80>(cfg, tm, tmt, tmo, size, t, H, n_items, o, scale_log2, L)
+                        : launch_attn_tc<false, 80>(cfg, tm, tmt, tmo, size, t, H, n_items, o, scale_log2, L);
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 

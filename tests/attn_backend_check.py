@@ -22,10 +22,11 @@ def ref(qkv, size, b, t, heads, hd):
 def main():
     lib = _cuda.lib()
     st = torch.cuda.current_stream().cuda_stream
-    shapes = [(7, 1), (5, 33), (6, 64), (4, 65), (3, 197), (2, 300), (2, 513), (2, 581)]
-    for b, t in shapes:
+    shapes = [(7, 1, 64), (5, 33, 64), (6, 64, 64), (4, 65, 64), (3, 197, 64), (2, 300, 64), (2, 513, 64),
+              (2, 581, 64), (5, 65, 80), (4, 185, 80), (3, 233, 80), (3, 257, 80), (2, 300, 80)]
+    for b, t, hd in shapes:
         for with_size in (False, True):
-            heads, hd = 12, 64
+            heads = 12 if hd == 64 else 16
             g = torch.Generator(device="cuda").manual_seed(t * 31 + b)
             qkv = (torch.randn(b, t, 3 * heads * hd, device="cuda", generator=g) * 1.5).bfloat16()
             size = torch.randint(1, 7, (b, t), device="cuda", generator=g).float() if with_size else None
@@ -37,7 +38,7 @@ def main():
             # bf16 output: |err| <= 2e-2 + 2e-2 |ref| (torch.testing.assert_close form)
             excess = ((out.double() - r).abs() - (2e-2 + 2e-2 * r.abs())).max().item()
             err = (out.double() - r).abs().max().item()
-            print(f"{os.environ.get('TA_ATTENTION_BACKEND', 'default')} b={b} t={t} size={with_size} "
+            print(f"{os.environ.get('TA_ATTENTION_BACKEND', 'default')} b={b} t={t} hd={hd} size={with_size} "
                   f"max|err|={err:.3e} excess={excess:.3e}")
             if not excess <= 0:
                 sys.exit(1)
