@@ -322,7 +322,19 @@ def dominant_gemm(cfg, B, dev, peak):
     e1.synchronize()
     ms = e0.elapsed_time(e1) / n
     tf = 2.0 * M * N * K / (ms / 1e3) / 1e12
+    traffic = None  # DRAM bytes per launch from the committed `ncu --set full` capture of this shape
+    try:
+        import glob
+        import re
+
+        prof = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_gemm_fc1.txt")))[-1]
+        vals = {k: float(v) for k, v in re.findall(r"(dram__bytes_(?:read|write)\.sum)\s+([0-9.]+)", open(prof).read())}
+        traffic = {"bytes": round((vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]) * 1e6),
+                   "algorithmic_bytes": 2 * (M * K + N * K + M * N), "source": os.path.basename(prof)}
+    except Exception:
+        pass
     return {"kernel": "gemm_bf16_sm100_pair_kernel<EPI_BIAS_GELU> (fc1 shape, timed alone via ta_gemm)", "shape": [M, N, K],
+            "traffic": traffic,
             "ms": round(ms, 4), "achieved": round(tf, 1), "unit": "TFLOP/s", "peak": peak,
             "frac": round(tf / peak, 4), "bound": "tensor"}
 
