@@ -21,6 +21,15 @@ __global__ void rate(float* out, unsigned long long* clk, int iters) {
       if (kMode == 0) v[i] = ex2(v[i]) * -0.5f;       // MUFU + FMUL
       if (kMode == 1) w[i] = ffma2(w[i], a, b);        // FFMA2
       if (kMode == 2) { v[i] = ex2(v[i]) * -0.5f; w[i] = ffma2(w[i], a, b); w[i] = ffma2(w[i], a, b); }
+      if (kMode == 3) {  // bf16x2 pack only (F2FP): which pipe, what rate
+        uint32_t p; asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(v[i]), "f"(v[(i + 1) & 7]));
+        v[i] = __uint_as_float(p) * 1.0001f;
+      }
+      if (kMode == 4) {  // ex2 + one pack per element pair
+        v[i] = ex2(v[i]) * -0.5f;
+        uint32_t p; asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(v[i]), "f"(v[(i + 1) & 7]));
+        w[i] ^= p;
+      }
     }
   }
   const unsigned long long t1 = clock64();
@@ -49,5 +58,7 @@ int main() {
   for (int w : {4, 8, 16}) run<0>("ex2 (+fmul)", w, d, c);
   for (int w : {4, 8, 16}) run<1>("ffma2 (pairs)", w, d, c);
   for (int w : {8, 16}) run<2>("mix ex2 + 2 ffma2", w, d, c);
+  for (int w : {8, 16}) run<3>("bf16x2 pack (+fmul)", w, d, c);
+  for (int w : {8, 16}) run<4>("ex2 + bf16x2 pack", w, d, c);
   return 0;
 }
