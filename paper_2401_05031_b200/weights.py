@@ -18,7 +18,8 @@ import torch
 
 from .config import ViTConfig
 
-__all__ = ["init_backbone", "init_head", "init_prompts", "synthetic_images"]
+__all__ = ["init_backbone", "init_head", "init_prompts", "synthetic_images", "from_timm_state_dict",
+           "to_timm_state_dict", "load_checkpoint"]
 
 
 def _trunc_normal(shape, std: float, g: torch.Generator) -> torch.Tensor:
@@ -90,3 +91,67 @@ def synthetic_images(batch: int, img: int, seed: int = 0,
     """Normalised-image-like N(0, 1) inputs [B, 3, img, img] fp32."""
     g = torch.Generator(device=device or "cpu").manual_seed(seed)
     return torch.randn(batch, 3, img, img, generator=g, device=device)
+
+
+# ----------------------------------------------------------------------------- checkpoints
+# timm VisionTransformer state-dict names (the paper's backbone, PAPER.md:533) <-> the layout
+# above.  Heads: timm's `head.weight` / `head.bias` become one TaskModel head; VPT-deep prompt
+# tensors ([L, gamma, D], PAPER.md:273-279) are used as they are.
+_TIMM_LAYER = {
+    "ln1_w": "norm1.weight", "ln1_b": "norm1.bias", "qkv_w": "attn.qkv.weight", "qkv_b": "attn.qkv.bias",
+    "proj_w": "attn.proj.weight", "proj_b": "attn.proj.bias", "ln2_w": "norm2.weight", "ln2_b": "norm2.bias",
+    "fc1_w": "mlp.fc1.weight", "fc1_b": "mlp.fc1.bias", "fc2_w": "mlp.fc2.weight", "fc2_b": "mlp.fc2.bias",
+}
+
+
+def from_timm_state_dict(sd: Dict[str, torch.Tensor], cfg: ViTConfig) -> Dict[str, object]:
+    """timm ``vit_*_patch*_224`` state dict -> fp32 master weights for TransformerModel.
+    Raises KeyError naming the first missing tensor and ValueError on a shape mismatch."""
+    def get(name, shape):
+        t = sd[name].detach().to("cpu", torch.float32)
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+        return t.contiguous()
+
+    d, p, n = cfg.dim, cfg.patch, cfg.n_tokens
+    params: Dict[str, object] = {
+        "patch_w": get("patch_embed.proj.weight", (d, 3, p, p)),
+        "patch_b": get("patch_embed.proj.bias", (d,)),
+        "cls": get("cls_token", (1, 1, d)).reshape(d),
+        "pos": get("pos_embed", (1, n, d)).reshape(n, d),
+        "norm_w": get("norm.weight", (d,)),
+        "norm_b": get("norm.bias", (d,)),
+    }
+    shapes = {"ln1_w": (d,), "ln1_b": (d,), "qkv_w": (3 * d, d), "qkv_b": (3 * d,), "proj_w": (d, d),
+              "proj_b": (d,), "ln2_w": (d,), "ln2_b": (d,), "fc1_w": (cfg.mlp_dim, d), "fc1_b": (cfg.mlp_dim,),
+              "fc2_w": (d, cfg.mlp_dim), "fc2_b": (d,)}
+    params["layers"] = [{k: get(f"blocks.{i}.{v}", shapes[k]) for k, v in _TIMM_LAYER.items()}
+                        for i in range(cfg.depth)]
+    return params
+
+
+def to_timm_state_dict(params: Dict[str, object], cfg: ViTConfig) -> Dict[str, torch.Tensor]:
+    """Inverse of ``from_timm_state_dict`` (backbone tensors only)."""
+    d, n = cfg.dim, cfg.n_tokens
+    sd = {"patch_embed.proj.weight": params["patch_w"], "patch_embed.proj.bias": params["patch_b"],
+          "cls_token": params["cls"].reshape(1, 1, d), "pos_embed": params["pos"].reshape(1, n, d),
+          "norm.weight": params["norm_w"], "norm.bias": params["norm_b"]}
+    for i, lw in enumerate(params["layers"]):
+        for k, v in _TIMM_LAYER.items():
+            sd[f"blocks.{i}.{v}"] = lw[k]
+    return sd
+
+
+def load_checkpoint(path: str, cfg: ViTConfig) -> Dict[str, object]:
+    """A timm checkpoint file (torch.save state dict, optionally under "model" / "state_dict";
+    .safetensors if the package is importable) -> master weights."""
+    if path.endswith(".safetensors"):
+        from safetensors.torch import load_file  # optional dependency
+
+        sd = load_file(path)
+    else:
+        sd = torch.load(path, map_location="cpu", weights_only=True)
+        for key in ("model", "state_dict"):
+            if isinstance(sd, dict) and key in sd and isinstance(sd[key], dict):
+                sd = sd[key]
+    return from_timm_state_dict(sd, cfg)
