@@ -266,59 +266,91 @@ int layernorm(const float* x, const float* w, const float* b, void* out, int row
 
 // ------------------------------------------------------------------ head
 // logits[b, c] = LN(x[b, 0, :]) . W_task[c] + b_task[c] for c < C_task, -inf beyond.
-__global__ void head_kernel(const float* __restrict__ x, int t_total, int D,
-                            const float* __restrict__ nw, const float* __restrict__ nb,
-                            const HeadDesc* __restrict__ heads, const int32_t* __restrict__ task,
-                            float* __restrict__ logits, int c_max) {
-  extern __shared__ float hrow[];
-  __shared__ float red[32];
-  const int b = blockIdx.x;
-  const float* xr = x + static_cast<long long>(b) * t_total * D;
+// Final LayerNorm of each image's class-token row + its task's linear head.  A CTA takes
+// kHeadImgs images x kHeadCls classes: one warp per image normalises its row into smem
+// (two-pass statistics), then for every task present among the images each warp owns classes
+// of the CTA's class chunk and dots each weight row with every image of that task, so a
+// head's weights are read once per kHeadImgs images instead of once per image.
+constexpr int kHeadImgs = 8;
+constexpr int kHeadCls = 16;
+__global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ x, int B, int t_total, int D,
+                                                   const float* __restrict__ nw, const float* __restrict__ nb,
+                                                   const HeadDesc* __restrict__ heads,
+                                                   const int32_t* __restrict__ task,
+                                                   float* __restrict__ logits, int c_max) {
+  extern __shared__ float hrow[];  // [kHeadImgs][D]
+  __shared__ int s_task[kHeadImgs];
+  grid_dep_wait();
+  grid_dep_launch();
+  const int b0 = blockIdx.x * kHeadImgs;
+  const int n_img = min(kHeadImgs, B - b0);
+  const int warp = static_cast<int>(warp_id()), lane = static_cast<int>(lane_id());
   const int nwarps = blockDim.x / 32;
-  float s = 0.f;
-  for (int c = threadIdx.x; c < D; c += blockDim.x) {
-    hrow[c] = xr[c];
-    s += hrow[c];
-  }
-  s = warp_sum(s);
-  if (lane_id() == 0) red[warp_id()] = s;
-  __syncthreads();
-  float tot = 0.f;
-  for (int i = 0; i < nwarps; ++i) tot += red[i];
-  const float mean = tot / D;
-  __syncthreads();
-  float q = 0.f;
-  for (int c = threadIdx.x; c < D; c += blockDim.x) {
-    const float d = hrow[c] - mean;
-    q += d * d;
-  }
-  q = warp_sum(q);
-  if (lane_id() == 0) red[warp_id()] = q;
-  __syncthreads();
-  float qt = 0.f;
-  for (int i = 0; i < nwarps; ++i) qt += red[i];
-  const float rstd = 1.0f / sqrtf(qt / D + 1e-6f);
-  for (int c = threadIdx.x; c < D; c += blockDim.x) hrow[c] = (hrow[c] - mean) * rstd * nw[c] + nb[c];
-  __syncthreads();
-  const HeadDesc h = heads[task[b]];
-  for (int c = warp_id(); c < c_max; c += nwarps) {
-    float acc = 0.f;
-    if (c < h.classes) {
-      const float* wr = h.w + static_cast<long long>(c) * D;
-      for (int k = lane_id(); k < D; k += 32) acc += hrow[k] * wr[k];
-      acc = warp_sum(acc);
-      acc += h.b[c];
-    } else {
-      acc = -INFINITY;
+  if (warp < n_img) {
+    const int b = b0 + warp;
+    const float* xr = x + static_cast<long long>(b) * t_total * D;  // class token = row 0
+    float* hr = hrow + warp * D;
+    float sm = 0.f;
+    for (int c = lane; c < D; c += 32) {
+      hr[c] = xr[c];
+      sm += hr[c];
     }
-    if (lane_id() == 0) logits[static_cast<long long>(b) * c_max + c] = acc;
+    const float mean = warp_sum(sm) / D;
+    float q = 0.f;
+    for (int c = lane; c < D; c += 32) {
+      const float d = hr[c] - mean;
+      q += d * d;
+    }
+    const float rstd = 1.0f / sqrtf(warp_sum(q) / D + 1e-6f);
+    for (int c = lane; c < D; c += 32) hr[c] = (hr[c] - mean) * rstd * nw[c] + nb[c];
+    if (lane == 0) s_task[warp] = task[b];
+  }
+  __syncthreads();
+  for (int j = 0; j < n_img; ++j) {
+    const int tk = s_task[j];
+    bool first = true;  // handle each distinct task once, at its first image
+    for (int jj = 0; jj < j; ++jj) first = first && s_task[jj] != tk;
+    if (!first) continue;
+    const HeadDesc h = heads[tk];
+    const int c_end = min(c_max, static_cast<int>(blockIdx.y + 1) * kHeadCls);
+    for (int c = static_cast<int>(blockIdx.y) * kHeadCls + warp; c < c_end; c += nwarps) {
+      if (c >= h.classes) {
+        for (int im = 0; im < n_img; ++im)
+          if (s_task[im] == tk && lane == 0) logits[static_cast<long long>(b0 + im) * c_max + c] = -INFINITY;
+        continue;
+      }
+      const float* wr = h.w + static_cast<long long>(c) * D;
+      for (int im = 0; im < n_img; ++im) {
+        if (s_task[im] != tk) continue;
+        const float* hr = hrow + im * D;
+        float acc = 0.f;
+        for (int k = lane; k < D; k += 32) acc += hr[k] * __ldg(wr + k);
+        acc = warp_sum(acc);
+        if (lane == 0) logits[static_cast<long long>(b0 + im) * c_max + c] = acc + h.b[c];
+      }
+    }
   }
 }
 
 int head(const float* x, int B, int t_total, int D, const float* nw, const float* nb,
          const HeadDesc* heads, const int32_t* task, float* logits, int c_max, cudaStream_t s) {
-  head_kernel<<<B, 256, D * sizeof(float), s>>>(x, t_total, D, nw, nb, heads, task, logits, c_max);
-  cudaError_t e = cudaGetLastError();
+  const size_t smem = static_cast<size_t>(kHeadImgs) * D * sizeof(float);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(smem));
+    if (e != cudaSuccess) return set_last_cuda_error(e);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((B + kHeadImgs - 1) / kHeadImgs, (c_max + kHeadCls - 1) / kHeadCls);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, head_kernel, x, B, t_total, D, nw, nb, heads, task, logits, c_max);
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 
