@@ -171,7 +171,9 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         dist.init_process_group("gloo")
-    dev = torch.device("cuda", local)
+    # one rank per GPU; if a box exposes fewer GPUs than ranks (multi-rank smoke tests on a
+    # single-GPU box) ranks share devices round-robin
+    dev = torch.device("cuda", local % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
 
     cfg, params = helpers.backbone(args.model)
@@ -219,7 +221,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize(dev)
     ev_list = []
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev.index) as clocks:
         for _ in range(args.steps):
             ev_list.append(step())
         torch.cuda.synchronize(dev)
