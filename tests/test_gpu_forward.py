@@ -135,3 +135,18 @@ def test_vit_h14_config5(dtype):
         torch.testing.assert_close(_finite(out), _finite(ref), rtol=1e-4, atol=1e-4 * scale)
     else:
         assert (_finite(forced) - _finite(ref)).abs().max().item() <= BF16_TOL * scale
+
+
+@pytest.mark.parametrize("batch", [1, 3])
+@pytest.mark.parametrize("gamma", [-8, 8])
+def test_vit_b16_odd_batches(batch, gamma):
+    """Batches that fill neither a 128-row tile nor a CTA pair (B*t not a multiple of 256),
+    bf16 index-forced and fp32 free-running (merge indices bit-exact)."""
+    cfg, ref, tr, out, gtr, forced, _ = _run("vit_b16", gamma, batch, "bf16")
+    rf = _finite(ref)
+    assert (_finite(forced) - rf).abs().max().item() <= BF16_TOL * rf.abs().max().item()
+    cfg, ref, tr, out, gtr, _, _ = _run("vit_b16", gamma, batch, "fp32")
+    if gamma < 0:
+        _assert_indices_equal(tr, gtr)
+    scale = _finite(ref).abs().max().item()
+    torch.testing.assert_close(_finite(out), _finite(ref), rtol=1e-4, atol=1e-4 * scale)
