@@ -1136,7 +1136,15 @@ int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, b
   if (K % kBK != 0 || N % 128 != 0) return TA_ERR_SHAPE;
   if ((epi_is_resid(epi_kind) || epi_is_patch(epi_kind)) && out_bf16) return TA_ERR_INVALID;
   if (epi_is_ln(epi_kind) && !out_bf16) return TA_ERR_INVALID;
-  const int BN = (N % 256 == 0) ? 256 : 128;
+  static const int force_bn = [] {  // profiling: TA_GEMM_BN=128 forces the 128 x 128 kernel
+    const char* v = getenv("TA_GEMM_BN");
+    return v ? atoi(v) : 0;
+  }();
+  // Tiny M x narrow N (ViT tail layers after merging, e.g. M = 256 x 11, N = 768): the 128 x 128
+  // single-CTA kernel fills more SMs than 256 x 256 pair tiles (tools/gemm_small.py: proj 9.5 vs
+  // 14.8 us, fc2 18.1 vs 25.4 us at M = 2816); everywhere else the pair kernel wins.
+  const bool tiny = M <= 3072 && N <= 1024;
+  const int BN = (force_bn == 128 || tiny) ? 128 : (N % 256 == 0) ? 256 : 128;
   CUtensorMap ta_, tb_;
   int rc = make_tmap_bf16_2d(&ta_, A, M, K, kBM);
   if (rc) return rc;
