@@ -408,12 +408,17 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
 // 128-byte box of the output through a per-warp double-buffered smem staging box and a TMA
 // store (thread = row straight from tcgen05.ld: no transpose, no per-thread global stores,
 // rows >= M clipped by TMA); the others keep the transposed coalesced-store path.
+// One staging box per epilogue warp leaves room for a sixth 32 KB mainloop stage (measured,
+// 3 interleaved runs: qkv 131.8 -> 129.0 us, fc2 192.8 -> 190.7 us, proj 83.5 -> 84.1 us).
+#ifndef TA_GEMM_BUFS
+#define TA_GEMM_BUFS 1
+#endif
 template <int EPI, typename OutT, bool kRemap>
 struct PairCfg {
   static constexpr bool kTma = pair_tma(EPI, kRemap);
   // (16 epilogue warps with one box each measured slower than 8 with two: register spills)
   static constexpr int kWarps = pair_epi_warps(EPI, kRemap);
-  static constexpr int kBufs = 2;  // staging boxes per epilogue warp
+  static constexpr int kBufs = TA_GEMM_BUFS;  // staging boxes per epilogue warp
   static constexpr int kThreads = 128 + 32 * kWarps;
   static constexpr int kABytes = 128 * kBK * 2;
   static constexpr int kBBytes = 128 * kBK * 2;  // this CTA's half of the 256-row W tile
