@@ -65,6 +65,7 @@ struct AttnTcLayout {
   int n_kv;     // K/V ring slots (2 when t_pad <= 256)
   int n_s;      // TMEM S slots (2 when t_pad <= 256)
   int rowsplit; // 1: softmax group g owns every other tile (t_pad <= 128); 0: groups split keys
+  int o_col;    // single S slot with O in its own TMEM columns [o_col, o_col + hd) (0: O aliases S)
   uint32_t kv_bytes;  // per slot: K then V
   uint32_t kv_off, p_off, bias_off, red_off, bar_off, smem_bytes;
 };
@@ -91,6 +92,13 @@ AttnTcLayout attn_layout(int t, int hd) {
   L.rowsplit = L.t_pad <= 256;
   if (const char* e = getenv("TA_ATTN_SPLIT"))  // profiling override: "row" / "key"
     L.rowsplit = L.t_pad <= 256 && e[0] != 'k';
+  // One S slot (t_pad > 256): when S and O fit side by side, O gets its own columns, the slot
+  // is released as soon as pass 2 has read it, and S of the next tile overlaps the PV tail and
+  // the (deferred) epilogue, as in two-slot mode.
+  L.o_col = 0;
+  if (L.n_s == 1 && L.t_pad <= 512 - ((hd + 15) / 16) * 16) L.o_col = 512 - ((hd + 15) / 16) * 16;
+  if (const char* e = getenv("TA_ATTN_OAPART"))  // profiling override: "0" keeps O aliased
+    if (e[0] == '0') L.o_col = 0;
   // K/V slot: [K main blocks][V main blocks][K tails][V tails]
   L.kt_off = 2u * L.n_kb * kBlkBytes;
   L.vt_off = L.kt_off + L.n_kb * L.tail_blk;
@@ -130,7 +138,10 @@ __device__ unsigned int g_trace_tag[16384];
 #define TRACE_DECL do {} while (0)
 #endif
 
-template <bool kHasSize, int kHD>
+// kOne: one K/V slot (L.n_kv == 1), where K and V have separate barriers and lifetimes and a
+// single S slot may keep O in its own TMEM columns (L.o_col); a template parameter so that the
+// two-slot instance carries none of that state (its register budget is tight).
+template <bool kHasSize, int kHD, bool kOne>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmt,
                    const __grid_constant__ CUtensorMap tmo,
@@ -142,6 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   constexpr int kTail = kHD - kHd;  // 16-column SW32 tail of a head_dim = 80 row (0 for 64)
+  const uint32_t o_col = kOne ? static_cast<uint32_t>(L.o_col) : 0u;
   const int D = H * kHD;
   uint8_t* sQ = smem;
   uint8_t* sKV = smem + L.kv_off;
@@ -149,8 +161,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* bias = reinterpret_cast<float*>(smem + L.bias_off);
   float* red = reinterpret_cast<float*>(smem + L.red_off);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
-  uint64_t* kv_full = bars + 0;   // [2]
-  uint64_t* kv_free = bars + 2;   // [2]
+  // K and V of an item have separate lifetimes: K is free once the item's last S MMA is done,
+  // V after its last PV, so with one K/V slot the next item's K (and first S) need not wait
+  // for the PV tail of the previous item.
+  uint64_t* kv_full = bars + 0;   // [2] K of the slot landed
+  uint64_t* kv_free = bars + 2;   // [2] K of the slot consumed
+  uint64_t* v_full = bars + 22;   // [2]
+  uint64_t* v_free = bars + 24;   // [2]
   uint64_t* q_full = bars + 4;    // [2]
   uint64_t* q_free = bars + 6;    // [2]
   uint64_t* s_full = bars + 8;    // [2]
@@ -158,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* o_full = bars + 12;   // [2]
   uint64_t* p_full = bars + 14;   // [4]
   uint64_t* p_free = bars + 18;   // [4]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   // No runtime integer division in the loops below: it compiles to I2F / MUFU.RCP / F2I on
@@ -184,6 +201,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_free[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_free[s], 1);
       mbar_init(&q_full[s], 1);
       mbar_init(&q_free[s], 1);
       mbar_init(&s_full[s], 1);
@@ -219,17 +238,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* sK = sKV + kvs * L.kv_bytes;
         uint8_t* sV = sK + L.n_kb * kBlkBytes;
         TRACE(1);
-        mbar_arrive_expect_tx(&kv_full[kvs], L.kv_bytes);
+        // Two slots: K and V share kv_full / kv_free (the ring runs an item ahead anyway).  One
+        // slot: V has its own barriers and is loaded after the item's first Q.
+        constexpr bool split_v = kOne;
+        const uint32_t half_bytes = L.n_kb * (kBlkBytes + L.tail_blk);
+        auto load_v = [&](uint64_t* bar) {
+          for (int kb = 0; kb < L.n_kb; ++kb) {
+            tma_load_2d(&tm, bar, sV + kb * kBlkBytes, 2 * D + h * kHD, row_base + kb * kKeyBlk);
+            if constexpr (kTail > 0)
+              tma_load_2d(&tmt, bar, sK + L.vt_off + kb * L.tail_blk, 2 * D + h * kHD + kHd,
+                          row_base + kb * kKeyBlk);
+          }
+        };
+        mbar_arrive_expect_tx(&kv_full[kvs], split_v ? half_bytes : 2 * half_bytes);
         for (int kb = 0; kb < L.n_kb; ++kb) {
           tma_load_2d(&tm, &kv_full[kvs], sK + kb * kBlkBytes, D + h * kHD, row_base + kb * kKeyBlk);
-          tma_load_2d(&tm, &kv_full[kvs], sV + kb * kBlkBytes, 2 * D + h * kHD, row_base + kb * kKeyBlk);
-          if constexpr (kTail > 0) {
+          if constexpr (kTail > 0)
             tma_load_2d(&tmt, &kv_full[kvs], sK + L.kt_off + kb * L.tail_blk, D + h * kHD + kHd,
                         row_base + kb * kKeyBlk);
-            tma_load_2d(&tmt, &kv_full[kvs], sK + L.vt_off + kb * L.tail_blk, 2 * D + h * kHD + kHd,
-                        row_base + kb * kKeyBlk);
-          }
         }
+        if (!split_v) load_v(&kv_full[kvs]);
         for (int qt = 0; qt < L.n_qt; ++qt, ++qcnt) {
           mbar_wait(&q_free[0], (qcnt & 1) ^ 1);
 #ifdef TA_ATTN_EXP_QONCE  // profiling only: wrong results (Q of the first tile reused)
@@ -244,6 +272,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         row_base + qt * kQTile + 64);
           }
           TRACE(2);
+          if (qt == 0 && split_v) {
+            mbar_wait(&v_free[kvs], (kv_use & 1) ^ 1);
+            mbar_arrive_expect_tx(&v_full[kvs], half_bytes);
+            load_v(&v_full[kvs]);
+          }
         }
       }
     }
@@ -272,16 +305,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t p_use[2] = {0, 0};  // per softmax group; stage = 2 g + (use & 1)
       // pending PV tile (issued after the next tile's S so softmax never waits)
       int pend_slot = -1, pend_kvs = 0;
-      bool pend_last = false;
-      auto issue_pv = [&](int sslot, int kvs, bool last_of_item) {
+      bool pend_last = false, pend_first = false;
+      uint32_t pend_vpar = 0;
+      auto issue_pv = [&](int sslot, int kvs, bool last_of_item, bool first_of_item, uint32_t v_par) {
         const uint8_t* sKVslot = sKV + kvs * L.kv_bytes;
-        const uint32_t o_tmem = tmem + sslot * 256;
+        const uint32_t o_tmem = o_col ? tmem + o_col : tmem + sslot * 256;
+        if (first_of_item && kOne) mbar_wait(&v_full[kvs], v_par);
         for (int kb = 0; kb < L.n_kb; ++kb) {
           const int grp = kb & 1;
           const uint32_t u = p_use[grp]++;
           const int ps = 2 * grp + (u & 1);
           mbar_wait(&p_full[ps], (u >> 1) & 1);
-          if (kTail > 0 && kb == 0 && L.n_kb > 1)  // O[0, 80) overlaps S block 1: wait for its P
+          if (kTail > 0 && kb == 0 && L.n_kb > 1 && !o_col)  // O[0, 80) overlaps S block 1: wait for its P
             mbar_wait(&p_full[2 + (p_use[1] & 1)], (p_use[1] >> 1) & 1);
           TRACE(5);
           tc_fence_after();
@@ -292,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         umma_commit(&o_full[sslot]);
         TRACE(6);
-        if (last_of_item) umma_commit(&kv_free[kvs]);
+        if (last_of_item) umma_commit(kOne ? &v_free[kvs] : &kv_free[kvs]);
       };
       if (L.rowsplit) {
         // Row-split mode (t_pad <= 256): tile n lives in S slot n % 2 and is softmaxed by group
@@ -331,6 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                          umma_desc_sw32(smem_u32(sK + L.kt_off)), idesc_s, 1);
               umma_commit(&s_full[slot]);
               umma_commit(&q_free[0]);
+              if (kOne && s_qt + 1 == L.n_qt) umma_commit(&kv_free[kvs]);  // the item's K is consumed
               TRACE(4);
               ++sN;
               if (++s_qt == L.n_qt) {
@@ -349,10 +385,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (kTail > 0 && pkb[grp] == 0 && L.n_kb > 1 &&
                 !mbar_test(&p_full[2 * grp + ((u + 1) & 1)], ((u + 1) >> 1) & 1))
               continue;
+            const int kvs = ring_slot(p_it[grp], L.n_kv);
+            if (kOne && pkb[grp] == 0 && !mbar_test(&v_full[kvs], p_it[grp] & 1)) continue;
             TRACE(8 + 16 * grp);
             ++p_use[grp];
             tc_fence_after();
-            const int kvs = ring_slot(p_it[grp], L.n_kv);
             const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
             const int nkc = pkb[grp] == L.n_kb - 1 ? L.nkc_last : kKeyBlk / 16;
             pv_block(tmem + grp * 256, pdesc, sKV + kvs * L.kv_bytes, pkb[grp], nkc);
@@ -362,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               umma_commit(&o_full[grp]);
               TRACE(6);
               if (++kv_tiles[kvs] == L.n_qt) {  // every tile of the item has its PV issued
-                umma_commit(&kv_free[kvs]);
+                umma_commit(kOne ? &v_free[kvs] : &kv_free[kvs]);
                 kv_tiles[kvs] = 0;
               }
               pt[grp] += 2;
@@ -385,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int qt = 0; qt < L.n_qt; ++qt, ++qcnt, ++tcnt) {
           const int ss = ring_slot(tcnt, L.n_s);
           if (L.n_s == 1 && pend_slot >= 0) {  // single S slot: finish the previous tile first
-            issue_pv(pend_slot, pend_kvs, pend_last);
+            issue_pv(pend_slot, pend_kvs, pend_last, pend_first, pend_vpar);
             pend_slot = -1;
           }
           mbar_wait(&s_free[ss], (ring_use(tcnt, L.n_s) & 1) ^ 1);
@@ -408,13 +445,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma_commit(&s_full[ss]);
           TRACE(4);
           umma_commit(&q_free[0]);
-          if (pend_slot >= 0) issue_pv(pend_slot, pend_kvs, pend_last);
+          if (kOne && qt + 1 == L.n_qt) umma_commit(&kv_free[kvs]);  // the item's K is consumed
+          if (pend_slot >= 0) issue_pv(pend_slot, pend_kvs, pend_last, pend_first, pend_vpar);
           pend_slot = ss;
           pend_kvs = kvs;
           pend_last = qt + 1 == L.n_qt;
+          pend_first = qt == 0;
+          pend_vpar = kv_use & 1;
         }
       }
-      if (pend_slot >= 0) issue_pv(pend_slot, pend_kvs, pend_last);
+      if (pend_slot >= 0) issue_pv(pend_slot, pend_kvs, pend_last, pend_first, pend_vpar);
       }
     }
   } else {
@@ -491,6 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&p_full[pst]);
         TRACE(14);
       }
+      if (o_col) mbar_arrive(&s_free[0]);  // S fully read (tc_fence_before above): next S may go
       TRACE(15);
       sts_f32(s_red + (256 + g * 128 + i) * 4, f2_total(acc));
       named_bar_sync(1, 256);
@@ -514,11 +555,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       TRACE(17);
       tc_fence_after();
       uint32_t o[32], ot[16];
-      tmem_ld_32x32b_x32(lane_base + ss * 256 + g * 32, o);
-      if (kTail > 0 && g == 1) tmem_ld_32x32b_x16(lane_base + ss * 256 + kHd, ot);
+      const uint32_t o_base = lane_base + (o_col ? o_col : ss * 256);
+      tmem_ld_32x32b_x32(o_base + g * 32, o);
+      if (kTail > 0 && g == 1) tmem_ld_32x32b_x16(o_base + kHd, ot);
       tmem_ld_wait();
       tc_fence_before();
-      mbar_arrive(&s_free[ss]);
+      if (!o_col) mbar_arrive(&s_free[ss]);
       const int q0 = qt * kQTile + (warp & 3) * 32;
       if (q0 < t) store_o_slab(&tmo, o, inv, s_slab, lane, h * kHD + g * 32, q0, b);
       if (kTail > 0 && g == 1) store_o_tail(ot, inv, b, q0 + static_cast<int>(lane), h);
@@ -679,19 +721,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 int make_tmap_bf16_2d_sw(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                          uint32_t box_cols, uint32_t box_rows, int swizzle_bytes);
 
-template <bool kHasSize, int kHD>
+template <bool kHasSize, int kHD, bool kOne>
 static cudaError_t launch_attn_tc(const cudaLaunchConfig_t& cfg, const CUtensorMap& tm,
                                   const CUtensorMap& tmt, const CUtensorMap& tmo, const float* size,
                                   int t, int H, int n_items, __nv_bfloat16* o, float scale_log2,
                                   const AttnTcLayout& L) {
   static bool attr_set = false;
   if (!attr_set) {
-    const cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<kHasSize, kHD>,
+    const cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<kHasSize, kHD, kOne>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  return cudaLaunchKernelEx(&cfg, attn_tc_kernel<kHasSize, kHD>, tm, tmt, tmo, size, t, H, n_items, o,
+  return cudaLaunchKernelEx(&cfg, attn_tc_kernel<kHasSize, kHD, kOne>, tm, tmt, tmo, size, t, H, n_items, o,
                             scale_log2, L);
 }
 
@@ -727,12 +769,15 @@ int attention_tc(const void* qkv, const float* size, int B, int t, int H, int hd
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(hd));
   auto* o = static_cast<__nv_bfloat16*>(out);
   cudaError_t e;
+#define TA_ATTN_LAUNCH(S, HD, ONE) launch_attn_tc<S, HD, ONE>(cfg, tm, tmt, tmo, size, t, H, n_items, o, scale_log2, L)
+  const bool one = L.n_kv == 1, sz = size != nullptr;
   if (hd == 64)
-    e = size != nullptr ? launch_attn_tc<true, 64>(cfg, tm, tmt, tmo, size, t, H, n_items, o, scale_log2, L)
-                        : launch_attn_tc<false, 64>(cfg, tm, tmt, tmo, size, t, H, n_items, o, scale_log2, L);
+    e = one ? (sz ? TA_ATTN_LAUNCH(true, 64, true) : TA_ATTN_LAUNCH(false, 64, true))
+            : (sz ? TA_ATTN_LAUNCH(true, 64, false) : TA_ATTN_LAUNCH(false, 64, false));
   else
-    e = size != nullptr ? launch_attn_tc<true, 80>(cfg, tm, tmt, tmo, size, t, H, n_items, o, scale_log2, L)
-                        : launch_attn_tc<false, 80>(cfg, tm, tmt, tmo, size, t, H, n_items, o, scale_log2, L);
+    e = one ? (sz ? TA_ATTN_LAUNCH(true, 80, true) : TA_ATTN_LAUNCH(false, 80, true))
+            : (sz ? TA_ATTN_LAUNCH(true, 80, false) : TA_ATTN_LAUNCH(false, 80, false));
+#undef TA_ATTN_LAUNCH
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 

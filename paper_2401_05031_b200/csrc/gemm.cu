@@ -655,7 +655,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
             const float4* bp = reinterpret_cast<const float4*>(epi.bias + n0);
 #pragma unroll
             for (int j = 0; j < CW / 4; ++j) {
-              const float4 b = epi.skip == 3 ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(bp + j);
+              const float4 b = __ldg(bp + j);
               const float2 lo = f2_unpack(fadd2(f2_pack(v[4 * j], v[4 * j + 1]), f2_pack(b.x, b.y)));
               const float2 hi = f2_unpack(fadd2(f2_pack(v[4 * j + 2], v[4 * j + 3]), f2_pack(b.z, b.w)));
               v[4 * j] = lo.x;
@@ -1126,7 +1126,7 @@ static int dispatch_bf16(const CUtensorMap& a, const CUtensorMap& b, int M, int 
 int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, bool out_bf16,
               const GemmEpi& epi_in, cudaStream_t stream) {
   static const int skip_epi = [] {
-    // profiling only: 1 = mainloop + TMEM drain only, 2 = no TMA store, 3 = no bias loads
+    // profiling only: 1 = mainloop + TMEM drain only, 2 = no TMA store
     const char* v = getenv("TA_GEMM_SKIP_EPILOGUE");
     return v ? atoi(v) : 0;
   }();

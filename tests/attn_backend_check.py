@@ -22,7 +22,7 @@ def ref(qkv, size, b, t, heads, hd):
 def main():
     lib = _cuda.lib()
     st = torch.cuda.current_stream().cuda_stream
-    shapes = [(7, 1, 64), (5, 33, 64), (6, 64, 64), (4, 65, 64), (3, 197, 64), (2, 300, 64), (2, 513, 64),
+    shapes = [(7, 1, 64), (5, 33, 64), (6, 64, 64), (4, 65, 64), (3, 197, 64), (2, 261, 64), (2, 300, 64), (2, 389, 64), (2, 449, 64), (2, 513, 64),
               (2, 581, 64), (5, 65, 80), (4, 185, 80), (3, 233, 80), (3, 257, 80), (2, 300, 80)]
     for b, t, hd in shapes:
         for with_size in (False, True):
