@@ -171,8 +171,11 @@ int match(const float* metric, const void* qkv, int qkv_dtype, int B, int t, int
 
 // ------------------------------------------------------------------ merge + LN2
 // grid (B, ceil(t'/ROWS)); one warp per output row; VEC float4 per lane (D = 128 VEC).
+// 3 CTAs per SM (register cap 85): more rows' loads in flight, merge 592 -> 524 us per ViT-B/16
+// forward at gamma = -16 and 772 -> 676 us at -8 (1 or 4 CTAs per SM, or two rows per warp
+// iteration, measured slower).
 template <int VEC, typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
     merge_kernel(const float* __restrict__ x, const float* __restrict__ size, int t, int r,
                  const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                  const int32_t* __restrict__ unm, const float* __restrict__ ln_w,
