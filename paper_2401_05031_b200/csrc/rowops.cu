@@ -122,50 +122,61 @@ int patchify(const float* img, void* out, int B, int S, int P, int Kp, int dtype
 // x is [B, t_total, D] fp32.  If cls != null: row 0 = cls + pos[0].  If gamma > 0: rows
 // [prompt_row, prompt_row + gamma) = prompts[task_b][layer] (a [gamma, D] block found via
 // the per-task pointer table; prompts are fp32 [depth, gamma, D]).
-__global__ void insert_rows_kernel(float* __restrict__ x, int t_total, int D,
+template <int VEC>
+__global__ void insert_rows_kernel(float* __restrict__ x, int t_total,
                                    const float* __restrict__ cls, const float* __restrict__ pos,
                                    const float* const* __restrict__ prompt_tab,
                                    const int32_t* __restrict__ task_ids, int layer, int gamma,
                                    int prompt_row, __nv_bfloat16* __restrict__ xh,
-                                   float* __restrict__ stats, int stat_slots) {
-  // One warp per inserted row; with xh / stats (LayerNorm folded into the QKV GEMM) the
-  // row is also written as bf16 and its exact (sum, sumsq) stored.
+                                   float* __restrict__ stats) {
+  // One warp per inserted row, VEC float4 per lane (D = 128 VEC), all loads before the stores;
+  // with xh / stats (LayerNorm folded into the QKV GEMM) the row is also written as bf16 and
+  // its exact (sum, sumsq) stored.  The previous kernel may have written the prompt slots
+  // (row-remapped TMA boxes), so nothing is stored before grid_dep_wait.
+  constexpr int D = 128 * VEC;
   const int b = blockIdx.x;
   const int n_cls = cls != nullptr ? 1 : 0;
   const int n_rows = n_cls + (gamma > 0 ? gamma : 0);
   const float* P = gamma > 0 ? prompt_tab[task_ids[b]] + static_cast<long long>(layer) * gamma * D
                              : nullptr;
   const int lane = lane_id();
+  grid_dep_wait();
+  grid_dep_launch();
   for (int rr = warp_id(); rr < n_rows; rr += blockDim.x / 32) {
     const bool is_cls = rr < n_cls;
     const long long row = static_cast<long long>(b) * t_total + (is_cls ? 0 : prompt_row + rr - n_cls);
-    const float* srow = is_cls ? nullptr : P + static_cast<long long>(rr - n_cls) * D;
-    float s = 0.f, q = 0.f;
-    for (int c = 4 * lane; c < D; c += 128) {
-      float4 v;
-      if (is_cls) {
-        const float4 a = *reinterpret_cast<const float4*>(cls + c);
-        const float4 p = *reinterpret_cast<const float4*>(pos + c);
-        v = make_float4(a.x + p.x, a.y + p.y, a.z + p.z, a.w + p.w);
-      } else {
-        v = *reinterpret_cast<const float4*>(srow + c);
+    float4 v[VEC];
+    if (is_cls) {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        const float4 a = reinterpret_cast<const float4*>(cls)[lane + 32 * i];
+        const float4 p = reinterpret_cast<const float4*>(pos)[lane + 32 * i];
+        v[i] = make_float4(a.x + p.x, a.y + p.y, a.z + p.z, a.w + p.w);
       }
-      *reinterpret_cast<float4*>(x + row * D + c) = v;
+    } else {
+      const float4* srow = reinterpret_cast<const float4*>(P + static_cast<long long>(rr - n_cls) * D);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) v[i] = srow[lane + 32 * i];
+    }
+    float s = 0.f, q = 0.f;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      reinterpret_cast<float4*>(x + row * D)[lane + 32 * i] = v[i];
       if (xh != nullptr) {
         uint2 pk;
-        pk.x = pack_bf16(v.x, v.y);
-        pk.y = pack_bf16(v.z, v.w);
-        *reinterpret_cast<uint2*>(xh + row * D + c) = pk;
-        s += (v.x + v.y) + (v.z + v.w);
-        q += (v.x * v.x + v.y * v.y) + (v.z * v.z + v.w * v.w);
+        pk.x = pack_bf16(v[i].x, v[i].y);
+        pk.y = pack_bf16(v[i].z, v[i].w);
+        reinterpret_cast<uint2*>(xh + row * D)[lane + 32 * i] = pk;
+        s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+        q += (v[i].x * v[i].x + v[i].y * v[i].y) + (v[i].z * v[i].z + v[i].w * v[i].w);
       }
     }
     if (stats != nullptr) {
       s = warp_sum(s);
       q = warp_sum(q);
       // whole-row sums in slot 0, the other 128-column slots zero (common.h GemmEpi::stats)
-      if (lane < stat_slots)
-        *reinterpret_cast<float2*>(stats + 2 * (row * stat_slots + lane)) =
+      if (lane < VEC)
+        *reinterpret_cast<float2*>(stats + 2 * (row * VEC + lane)) =
             lane == 0 ? make_float2(s, q) : make_float2(0.f, 0.f);
     }
   }
@@ -175,10 +186,30 @@ int insert_rows(float* x, int B, int t_total, int D, const float* cls, const flo
                 const float* const* prompt_tab, const int32_t* task_ids, int layer, int gamma,
                 int prompt_row, cudaStream_t s, void* xh, float* stats) {
   if (D % 128 != 0) return TA_ERR_SHAPE;
-  insert_rows_kernel<<<B, 256, 0, s>>>(x, t_total, D, cls, pos, prompt_tab, task_ids, layer,
-                                       gamma, prompt_row, static_cast<__nv_bfloat16*>(xh), stats,
-                                       D / 128);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(B);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  auto* h = static_cast<__nv_bfloat16*>(xh);
+  cudaError_t e;
+  switch (D / 128) {
+#define TA_INSERT_CASE(V) \
+  case V:                 \
+    e = cudaLaunchKernelEx(&cfg, insert_rows_kernel<V>, x, t_total, cls, pos, prompt_tab, task_ids, layer, gamma, prompt_row, h, stats); \
+    break;
+    TA_INSERT_CASE(2)
+    TA_INSERT_CASE(6)
+    TA_INSERT_CASE(8)
+    TA_INSERT_CASE(10)
+#undef TA_INSERT_CASE
+    default:
+      return TA_ERR_SHAPE;
+  }
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 
