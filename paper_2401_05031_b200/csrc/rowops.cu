@@ -317,23 +317,40 @@ __global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ x, 
   const int n_img = min(kHeadImgs, B - b0);
   const int warp = static_cast<int>(warp_id()), lane = static_cast<int>(lane_id());
   const int nwarps = blockDim.x / 32;
+  // D = 128 VEC with VEC <= 10 (ViT-B / L / H: 6 / 8 / 10): each lane's class-token values are
+  // loaded as up to 10 float4 at once (a loop of dependent global loads through shared
+  // memory cost ~30 us per forward).
+  constexpr int kMaxVec = 10;
+  const int vec = D / 128;
   if (warp < n_img) {
     const int b = b0 + warp;
-    const float* xr = x + static_cast<long long>(b) * t_total * D;  // class token = row 0
-    float* hr = hrow + warp * D;
+    const float4* xr = reinterpret_cast<const float4*>(x + static_cast<long long>(b) * t_total * D);
+    float4* hr = reinterpret_cast<float4*>(hrow + warp * D);
+    float4 v[kMaxVec];
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i)
+      if (i < vec) v[i] = xr[lane + 32 * i];
     float sm = 0.f;
-    for (int c = lane; c < D; c += 32) {
-      hr[c] = xr[c];
-      sm += hr[c];
-    }
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i)
+      if (i < vec) sm += (v[i].x + v[i].y) + (v[i].z + v[i].w);
     const float mean = warp_sum(sm) / D;
     float q = 0.f;
-    for (int c = lane; c < D; c += 32) {
-      const float d = hr[c] - mean;
-      q += d * d;
-    }
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i)
+      if (i < vec) {
+        const float a = v[i].x - mean, bb = v[i].y - mean, c = v[i].z - mean, d = v[i].w - mean;
+        q += (a * a + bb * bb) + (c * c + d * d);
+      }
     const float rstd = 1.0f / sqrtf(warp_sum(q) / D + 1e-6f);
-    for (int c = lane; c < D; c += 32) hr[c] = (hr[c] - mean) * rstd * nw[c] + nb[c];
+#pragma unroll
+    for (int i = 0; i < kMaxVec; ++i)
+      if (i < vec) {
+        const float4 g = __ldg(reinterpret_cast<const float4*>(nw) + lane + 32 * i);
+        const float4 o = __ldg(reinterpret_cast<const float4*>(nb) + lane + 32 * i);
+        hr[lane + 32 * i] = make_float4((v[i].x - mean) * rstd * g.x + o.x, (v[i].y - mean) * rstd * g.y + o.y,
+                                        (v[i].z - mean) * rstd * g.z + o.z, (v[i].w - mean) * rstd * g.w + o.w);
+      }
     if (lane == 0) s_task[warp] = task[b];
   }
   __syncthreads();
@@ -350,12 +367,21 @@ __global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ x, 
           if (s_task[im] == tk && lane == 0) logits[static_cast<long long>(b0 + im) * c_max + c] = -INFINITY;
         continue;
       }
-      const float* wr = h.w + static_cast<long long>(c) * D;
+      const float4* wr = reinterpret_cast<const float4*>(h.w + static_cast<long long>(c) * D);
+      float4 wv[kMaxVec];
+#pragma unroll
+      for (int i = 0; i < kMaxVec; ++i)
+        if (i < vec) wv[i] = __ldg(wr + lane + 32 * i);
       for (int im = 0; im < n_img; ++im) {
         if (s_task[im] != tk) continue;
-        const float* hr = hrow + im * D;
+        const float4* hr = reinterpret_cast<const float4*>(hrow + im * D);
         float acc = 0.f;
-        for (int k = lane; k < D; k += 32) acc += hr[k] * __ldg(wr + k);
+#pragma unroll
+        for (int i = 0; i < kMaxVec; ++i)
+          if (i < vec) {
+            const float4 hv = hr[lane + 32 * i];
+            acc += (hv.x * wv[i].x + hv.y * wv[i].y) + (hv.z * wv[i].z + hv.w * wv[i].w);
+          }
         acc = warp_sum(acc);
         if (lane == 0) logits[static_cast<long long>(b0 + im) * c_max + c] = acc + h.b[c];
       }
@@ -365,6 +391,7 @@ __global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ x, 
 
 int head(const float* x, int B, int t_total, int D, const float* nw, const float* nb,
          const HeadDesc* heads, const int32_t* task, float* logits, int c_max, cudaStream_t s) {
+  if (D % 128 != 0 || D > 1280) return TA_ERR_SHAPE;
   const size_t smem = static_cast<size_t>(kHeadImgs) * D * sizeof(float);
   if (smem > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
