@@ -57,17 +57,22 @@ __global__ void __launch_bounds__(256) patchify_kernel(const float* __restrict__
                                                        T* __restrict__ out, int B, int S, int P_rt,
                                                        int Kp) {
   const int P = kP ? kP : P_rt;
-  const int G = S / P, segs = 3 * P;
-  const int n = B * G * G * segs;  // < 2^31 (checked by the launcher)
+  const int G = S / P;
+  const int n = B * G * G * 3 * P;  // < 2^31 (checked by the launcher)
   grid_dep_wait();
   grid_dep_launch();
+  // idx walks the image in memory order (b, c, py, ky, px): a warp reads whole image rows.
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
-    const int patch = idx / segs;  // b * G * G + py * G + px
-    const int seg = idx - patch * segs;  // c * P + ky
-    const int b = patch / (G * G);
-    const int pp = patch - b * G * G;
-    const int py = pp / G, px = pp - py * G;
-    const int c = seg / P, ky = seg - c * P;
+    int r = idx / G;
+    const int px = idx - r * G;
+    int r2 = r / P;
+    const int ky = r - r2 * P;
+    r = r2 / G;
+    const int py = r2 - r * G;
+    const int b = r / 3;
+    const int c = r - b * 3;
+    const int patch = (b * G + py) * G + px;
+    const int seg = c * P + ky;
     const float* src = img + ((static_cast<long long>(b) * 3 + c) * S + py * P + ky) * S + px * P;
     T* row = out + static_cast<long long>(patch) * Kp;
     T* dst = row + seg * P;
