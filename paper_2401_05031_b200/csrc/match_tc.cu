@@ -31,6 +31,20 @@ __device__ __forceinline__ float tf32_trunc(float x) {
 
 constexpr int kFusedThreads = 512;
 
+#ifdef TA_MATCH_TRACE  // profiling build only: phase timestamps (globaltimer) of every CTA
+__device__ unsigned long long g_match_trace[4096][6];
+#define MTRACE(k)                                                                    \
+  do {                                                                               \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {                                     \
+      unsigned long long t_;                                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                         \
+      g_match_trace[blockIdx.x][k] = t_;                                             \
+    }                                                                                \
+  } while (0)
+#else
+#define MTRACE(k) do {} while (0)
+#endif
+
 // One CTA per image, 16 warps.  Phase 1 (all warps): metric row of every token (mean over
 // heads of k in fixed head order, or the given fp32 metric), x / ||x||_2, 3xTF32 split
 // x = hi + lo, written straight into the four SW128 K-major smem tiles the MMA reads (A_hi,
@@ -61,6 +75,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   const uint32_t warp = warp_id(), lane = lane_id();
   const uint32_t s0 = smem_u32(smem);
 
+  MTRACE(0);
   if (tid == 0) {
     mbar_init(bar_mma, 1);
     fence_barrier_init();
@@ -68,6 +83,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   if (warp == 0) tmem_alloc<128>(tmem_slot);
   grid_dep_wait();    // qkv comes from the previous kernels
   grid_dep_launch();  // early trigger: the next kernel's prologue overlaps our tail
+  MTRACE(1);
 
   // ---- phase 1: metric rows -> normalised, split, swizzled smem tiles
   const long long D = static_cast<long long>(heads) * c;
@@ -85,6 +101,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       constexpr int kPP = 1;  // (2 row groups in flight spill at 16 heads x 16 bytes)
       const int seg = static_cast<int>(lane) / kSeg, sl = static_cast<int>(lane) % kSeg;
       const int j = 8 * sl;  // first column of this lane
+      // bf16 path: reciprocal multiplies instead of IEEE divisions (the fp32 path below keeps
+      // the oracle's exact mean / norm divisions)
+      const float inv_heads = 1.f / static_cast<float>(heads);
       constexpr int kStep = kRowsPerWarp * (kFusedThreads / 32);
       for (int t0 = static_cast<int>(warp) * kRowsPerWarp; t0 < t; t0 += kPP * kStep) {
         uint4 raw[kPP][16];
@@ -119,19 +138,19 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           float ss = 0.f;
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            a[e] /= heads;
+            a[e] *= inv_heads;
             ss += a[e] * a[e];
           }
 #pragma unroll
           for (int o = kSeg / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-          const float nrm = sqrtf(ss);
+          const float inv_nrm = rsqrtf(ss);
           if (tok < t && tok > 0 && j < cp) {
             const int ri = smem_row(tok);
             const uint32_t row_hi = s0 + ((tok & 1) * 2) * tile_bytes + ri * 128;
             float hv[8], lv[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-              const float x = j + e < c ? a[e] / nrm : 0.f;
+              const float x = j + e < c ? a[e] * inv_nrm : 0.f;
               hv[e] = tf32_trunc(x);
               lv[e] = tf32_trunc(x - hv[e]);
             }
@@ -209,6 +228,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  MTRACE(2);
   const uint32_t tmem = *tmem_slot;
 
   // ---- phase 2: S = A B^T in 3xTF32
@@ -262,6 +282,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  MTRACE(3);
   if (tid < na) {
     const int i = tid;
     const float vi = node_max[i];
@@ -286,6 +307,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     }
   }
   __syncthreads();
+  MTRACE(4);
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc<128>(tmem);
@@ -348,4 +370,10 @@ int match_tc(const float* metric, const void* qkv, int qkv_dtype, int B, int t, 
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 
+#ifdef TA_MATCH_TRACE
+extern "C" __attribute__((visibility("default"))) int ta_debug_match_trace(unsigned long long* out, int n) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, g_match_trace, static_cast<size_t>(n) * 6 * sizeof(unsigned long long)) == cudaSuccess ? 0 : -1;
+}
+#endif
 }  // namespace ta
