@@ -54,8 +54,12 @@ __device__ unsigned long long g_match_trace[4096][6];
 // Phase 2 (thread 0): S = A_hi B_hi^T + A_hi B_lo^T + A_lo B_hi^T, kind::tf32 into TMEM.
 // Phase 3 (warps 0..3, thread i = A row i = TMEM lane i): max / argmax over the B columns
 // (ties -> lowest column; the class token row is -inf), top-r by rank counting, unm ascending.
-template <typename QT, int kU>  // kU: 64-column passes per row (1: c <= 64, 2: c <= 128)
-__global__ void __launch_bounds__(kFusedThreads, 1)
+// kTerms = 3: S in 3xTF32 (fp32 mode: the oracle's decisions bit for bit); kTerms = 1: one
+// TF32 product (bf16 mode, where k itself is bf16: TF32's 2^-11 on the scores is below the
+// input's rounding), two smem tiles instead of four, 256 threads, two CTAs per SM so one
+// image's metric loads overlap another's MMA and selection.
+template <typename QT, int kU, int kTerms, int kThreads>  // kU: 64-column passes per row (1: c <= 64, 2: c <= 128)
+__global__ void __launch_bounds__(kThreads, kThreads == 256 ? 2 : 1)
     match_fused_kernel(const float* __restrict__ metric, const QT* __restrict__ qkv, int t,
                        int heads, int c, int cp, int r, int32_t* __restrict__ src_out,
                        int32_t* __restrict__ dst_out, int32_t* __restrict__ unm_out) {
@@ -66,7 +70,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   const int na = (t + 1) / 2, nb = t / 2;
   const int nkc = cp / 32;                   // 32-float K chunks (128-byte swizzle rows)
   const int tile_bytes = nkc * kRows * 128;  // one part
-  float* node_max = reinterpret_cast<float*>(smem + 4 * tile_bytes);
+  constexpr int kParts = kTerms == 3 ? 4 : 2;  // A_hi (A_lo) B_hi (B_lo)
+  constexpr int kBPart = kTerms == 3 ? 2 : 1;
+  float* node_max = reinterpret_cast<float*>(smem + kParts * tile_bytes);
   int* node_idx = reinterpret_cast<int*>(node_max + 2 * kRows);
   int* rank = node_idx + 2 * kRows;
   uint64_t* bar_mma = reinterpret_cast<uint64_t*>(rank + 2 * kRows);
@@ -104,7 +110,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       // bf16 path: reciprocal multiplies instead of IEEE divisions (the fp32 path below keeps
       // the oracle's exact mean / norm divisions)
       const float inv_heads = 1.f / static_cast<float>(heads);
-      constexpr int kStep = kRowsPerWarp * (kFusedThreads / 32);
+      constexpr int kStep = kRowsPerWarp * (kThreads / 32);
       for (int t0 = static_cast<int>(warp) * kRowsPerWarp; t0 < t; t0 += kPP * kStep) {
         uint4 raw[kPP][16];
 #pragma unroll
@@ -146,7 +152,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           const float inv_nrm = rsqrtf(ss);
           if (tok < t && tok > 0 && j < cp) {
             const int ri = smem_row(tok);
-            const uint32_t row_hi = s0 + ((tok & 1) * 2) * tile_bytes + ri * 128;
+            const uint32_t row_hi = s0 + ((tok & 1) * kBPart) * tile_bytes + ri * 128;
             float hv[8], lv[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
@@ -159,7 +165,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
             for (int h2 = 0; h2 < 2; ++h2) {
               const uint32_t off = kc * kRows * 128 + ((((jj >> 2) + h2) ^ (ri & 7)) << 4);
               sts_f4(row_hi + off, make_float4(hv[4 * h2], hv[4 * h2 + 1], hv[4 * h2 + 2], hv[4 * h2 + 3]));
-              sts_f4(row_hi + tile_bytes + off, make_float4(lv[4 * h2], lv[4 * h2 + 1], lv[4 * h2 + 2], lv[4 * h2 + 3]));
+              if constexpr (kTerms == 3)
+                sts_f4(row_hi + tile_bytes + off, make_float4(lv[4 * h2], lv[4 * h2 + 1], lv[4 * h2 + 2], lv[4 * h2 + 3]));
             }
           }
         }
@@ -167,7 +174,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     }
   }
   if (sizeof(QT) == 4 || metric != nullptr) {
-    for (int tok = static_cast<int>(warp); tok < t; tok += kFusedThreads / 32) {
+    for (int tok = static_cast<int>(warp); tok < t; tok += kThreads / 32) {
       float v[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
       float ss = 0.f;
   #pragma unroll
@@ -207,7 +214,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       const float nrm = sqrtf(warp_sum(ss));
       if (tok == 0) continue;  // the class token never enters the MMA (its S row is -inf)
       const int set = tok & 1, ri = smem_row(tok);
-      const uint32_t row_hi = s0 + (set * 2) * tile_bytes + ri * 128;
+      const uint32_t row_hi = s0 + (set * kBPart) * tile_bytes + ri * 128;
   #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int j = 2 * static_cast<int>(lane) + 64 * u;
@@ -219,7 +226,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           const int kc = j >> 5, jj = j & 31;
           const uint32_t off = kc * kRows * 128 + ((((jj >> 2) ^ (ri & 7))) << 4) + (jj & 3) * 4;
           asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(row_hi + off), "f"(h0), "f"(h1) : "memory");
-          asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(row_hi + tile_bytes + off), "f"(l0), "f"(l1) : "memory");
+          if constexpr (kTerms == 3)
+            asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(row_hi + tile_bytes + off), "f"(l0), "f"(l1) : "memory");
         }
       }
     }
@@ -235,9 +243,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   if (tid == 0) {
     constexpr uint32_t idesc = idesc_tf32(kRows, kRows);
     // (A part, B part): hi*hi, hi*lo, lo*hi
-    const int terms[3][2] = {{0, 2}, {0, 3}, {1, 2}};
+    const int terms[3][2] = {{0, kBPart}, {0, 3}, {1, 2}};
     int n = 0;
-    for (int tt = 0; tt < 3; ++tt) {
+    for (int tt = 0; tt < kTerms; ++tt) {
       for (int kc = 0; kc < nkc; ++kc) {
         const uint64_t ad = umma_desc_sw128(s0 + terms[tt][0] * tile_bytes + kc * kRows * 128);
         const uint64_t bd = umma_desc_sw128(s0 + terms[tt][1] * tile_bytes + kc * kRows * 128);
@@ -344,28 +352,31 @@ int match_tc(const float* metric, const void* qkv, int qkv_dtype, int B, int t, 
   if (r <= 0 || r > na - 1 || t < 3) return TA_ERR_INVALID;
   if (t > 2 * kRows + 1 || c > 96 || c % 8 || heads > 16) return TA_ERR_SHAPE;
   const int cp = (c + 31) / 32 * 32;
-  const size_t smem = 4 * (cp / 32) * kRows * 128 + 3 * 2 * kRows * 4 + 64 + 1024;
+  const size_t tiles = static_cast<size_t>(cp / 32) * kRows * 128;
+  const size_t tail = 3 * 2 * kRows * 4 + 64 + 1024;
+  const size_t smem3 = 4 * tiles + tail, smem1 = 2 * tiles + tail;
   static bool attr_set = false;
   cudaError_t e;
   if (!attr_set) {
-    e = cudaFuncSetAttribute(match_fused_kernel<float, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    e = cudaFuncSetAttribute(match_fused_kernel<float, 2, 3, kFusedThreads>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(match_fused_kernel<__nv_bfloat16, 1>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      e = cudaFuncSetAttribute(match_fused_kernel<__nv_bfloat16, 1, 1, 256>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(match_fused_kernel<__nv_bfloat16, 2>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      e = cudaFuncSetAttribute(match_fused_kernel<__nv_bfloat16, 2, 1, 256>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
     if (e != cudaSuccess) return set_last_cuda_error(e);
     attr_set = true;
   }
   if (metric != nullptr || qkv_dtype == TA_DTYPE_F32)
-    e = launch_pdl(match_fused_kernel<float, 2>, dim3(B), dim3(kFusedThreads), smem, s, metric,
-                   static_cast<const float*>(qkv), t, heads, c, cp, r, src, dst, unm);
+    e = launch_pdl(match_fused_kernel<float, 2, 3, kFusedThreads>, dim3(B), dim3(kFusedThreads), smem3, s,
+                   metric, static_cast<const float*>(qkv), t, heads, c, cp, r, src, dst, unm);
   else if (c <= 64)
-    e = launch_pdl(match_fused_kernel<__nv_bfloat16, 1>, dim3(B), dim3(kFusedThreads), smem, s, metric,
+    e = launch_pdl(match_fused_kernel<__nv_bfloat16, 1, 1, 256>, dim3(B), dim3(256), smem1, s, metric,
                    static_cast<const __nv_bfloat16*>(qkv), t, heads, c, cp, r, src, dst, unm);
   else
-    e = launch_pdl(match_fused_kernel<__nv_bfloat16, 2>, dim3(B), dim3(kFusedThreads), smem, s, metric,
+    e = launch_pdl(match_fused_kernel<__nv_bfloat16, 2, 1, 256>, dim3(B), dim3(256), smem1, s, metric,
                    static_cast<const __nv_bfloat16*>(qkv), t, heads, c, cp, r, src, dst, unm);
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
