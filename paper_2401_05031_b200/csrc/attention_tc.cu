@@ -9,19 +9,25 @@
 // Persistent, warp-specialised, one CTA per SM looping over work items (image, head); each
 // item walks its 128-query tiles with K / V fetched from HBM once per item.
 //   warp 8 (lane 0)  TMA producer: K, V of the item (64-row SW128 boxes) into a 2-slot
-//                    ring (1 slot when t > 256), Q tiles into a 2-slot ring.
+//                    ring (1 slot when t > 256: then K and V have their own barriers, K is
+//                    refilled after the item's last S and V after its last PV), Q tiles into
+//                    one slot.
 //   warp 9 (lane 0)  MMA issuer: S = Q K^T (M = 128, N <= 256 per instruction) into one of
 //                    two TMEM S slots; S of tile n+1 is issued before PV of tile n so the
 //                    softmax warps never wait for it; O += P_blk V_blk per 64-key block with
 //                    V as an MN-major B operand.
-//   warps 0..7       softmax in two groups over even / odd 64-key blocks; query row i is
+//   warps 0..7       t_pad <= 256 (row split): group g owns every other tile and its S slot,
+//                    whole rows per thread.  Otherwise softmax in two groups over even / odd
+//                    64-key blocks of one S slot; query row i is
 //                    TMEM lane i (warps w and w+4 share lanes 32(w%4)..); pass 1 row max m
 //                    of the raw scores, pass 2 p = size_j * 2^((s - m) log2(e)/sqrt(hd))
 //                    (= the log-size bias as a weight; size 0 masks keys >= t) -> bf16 P
 //                    block into ring stage g (SW128, K-major) -> PV MMA; row max / sum
 //                    combined through smem; epilogue O / sum -> bf16 rows.
 // TMEM: slot s at columns [256 s, 256 s + t_pad); O aliases the slot's S block 0, which
-// softmax has consumed before the first PV MMA is issued.  Keys past t are masked with a
+// softmax has consumed before the first PV MMA is issued -- except with one S slot and room
+// beside it (t_pad <= 512 - hd), where O has its own columns and the slot is released after
+// pass 2, so the next tile's S overlaps the PV tail and the epilogue.  Keys past t are masked with a
 // -inf bias (their K / V rows are the next image's rows or TMA zero fill: finite, p = 0).
 #include <cfloat>
 #include <cstdlib>
