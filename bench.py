@@ -11,8 +11,10 @@ ServeModel.forward with pinned host images (H2D + forward + D2H logits per batch
 
 Multi-GPU: one process per GPU (torchrun), full replica each, no collectives on the path
 (replicas only); value = all ranks' images / max-over-ranks time.
---impl reference times the CPU oracle (the reference has no implementation of the path,
-SURVEY.md §0; kind "port") on the host cores, rank 0 only.
+Started as `python bench.py --gpus N` (no launcher), it re-launches itself as N ranks through
+torch.distributed.run (replicas.launch_replicas).  --impl reference times the CPU oracle (the
+reference has no implementation of the path; kind "port") on the host cores,
+rank 0 only, one gamma of the sweep per step.
 """
 
 from __future__ import annotations
@@ -111,75 +113,206 @@ def launches_per_forward(cfg, gamma, prompt_mode="accumulate", fold_ln=True):
     return n
 
 
-def cpu_oracle_sample(cfg, params, tasks, batch, gammas, seed=0):
-    """Times the CPU oracle (fp32, all host threads) over one batch per gamma."""
-    from tests import helpers
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
 
-    n_threads = len(os.sched_getaffinity(0))
-    torch.set_num_threads(n_threads)
-    imgs = helpers.synthetic_images(batch, cfg.img, seed=seed)
-    ids = torch.zeros(batch, dtype=torch.int64)
-    t0 = time.perf_counter()
+    return platform.processor() or "unknown"
+
+
+class CpuOracle:
+    """The CPU reference of the path (oracle/vit_oracle.py, fp32 torch-CPU on all host threads):
+    the reference ships no implementation of the forward, so this port is its
+    CPU baseline.  Same seeded weights as the GPU replica (weights.py)."""
+
+    def __init__(self, model: str, gammas):
+        from paper_2401_05031_b200.config import VIT_CONFIGS
+        from paper_2401_05031_b200.synthetic import synthetic_task_params
+        from paper_2401_05031_b200.weights import init_backbone
+
+        self.cfg = VIT_CONFIGS[model]
+        self.params = init_backbone(self.cfg, 0)
+        self.tasks = synthetic_task_params(self.cfg, (100,), [g for g in gammas if g > 0])
+        self.cores = len(os.sched_getaffinity(0))
+        torch.set_num_threads(self.cores)
+
+    def run(self, batch: int, gamma: int, seed: int = 0) -> float:
+        """Seconds for one forward of `batch` synthetic images at `gamma`."""
+        from oracle import vit_oracle
+        from paper_2401_05031_b200.weights import synthetic_images
+
+        imgs = synthetic_images(batch, self.cfg.img, seed=seed)
+        ids = torch.zeros(batch, dtype=torch.int64)
+        heads = [t["head"] for t in self.tasks]
+        prompts = [t["prompts"].get(gamma) for t in self.tasks] if gamma > 0 else None
+        t0 = time.perf_counter()
+        with torch.inference_mode():
+            vit_oracle.forward(self.params, heads, imgs, ids, gamma, n_heads=self.cfg.heads,
+                               patch=self.cfg.patch, prompts=prompts)
+        return time.perf_counter() - t0
+
+
+def cpu_baseline(model, gammas, batch, config1=True):
+    """config 1 (b=8, gamma=-8) and one timed pass per gamma at the bench batch,
+    on this box's host cores."""
+    ora = CpuOracle(model, tuple(gammas) + ((-8,) if config1 else ()))
+    ora.run(1, 0)  # warm-up (thread pool, allocator)
+    out = {"unit": "images/s", "cores": ora.cores, "kind": "port", "cpu_model": cpu_model()}
+    if config1:
+        dt = ora.run(8, -8)
+        out["config1"] = {"workload": f"{model} batch 8 gamma=-8 (configs[0])", "images_per_s": round(8 / dt, 3)}
+    per, total_t = {}, 0.0
     for g in gammas:
-        helpers.oracle_forward(cfg, params, tasks, imgs, ids, g)
-    dt = time.perf_counter() - t0
-    return batch * len(gammas) / dt, n_threads, dt
+        dt = ora.run(batch, g)
+        per[str(g)] = round(batch / dt, 3)
+        total_t += dt
+    out["value"] = round(batch * len(gammas) / total_t, 3)
+    out["per_gamma"] = per
+    out["sample"] = (f"oracle/vit_oracle.py fp32 torch-CPU, one batch of {batch} per gamma {list(gammas)} "
+                     f"({total_t:.1f} s){' + config 1' if config1 else ''}")
+    return out
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle (port) on the host cores, bounded sample per step."""
-    from paper_2401_05031_b200.config import VIT_CONFIGS
-    from tests import helpers
-
+    """--impl reference: the CPU reference of the path on the host cores (rank 0 only).  Each
+    step is one batch of args.batch images at one gamma of the sweep, rotating through the
+    gammas (a whole sweep at b=256 would take minutes per step); value = images / seconds."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg, params = helpers.backbone(args.model)
-    tasks = helpers.task_params(cfg, (100,), [g for g in GAMMAS if g > 0])
-    sample_batch = args.ref_batch
-    for _ in range(args.warmup):
-        cpu_oracle_sample(cfg, params, tasks, 1, GAMMAS)
-    total_imgs, total_t, cores = 0, 0.0, 1
+    gammas = tuple(int(g) for g in args.gammas.split(",")) if args.gammas else GAMMAS
+    ora = CpuOracle(args.model, gammas)
+    for w in range(args.warmup):
+        ora.run(1, gammas[w % len(gammas)], seed=100 + w)
+    total_imgs, total_t, per = 0, 0.0, {}
     for s in range(args.steps):
-        ips, cores, dt = cpu_oracle_sample(cfg, params, tasks, sample_batch, GAMMAS, seed=s)
-        total_imgs += sample_batch * len(GAMMAS)
+        g = gammas[s % len(gammas)]
+        dt = ora.run(args.batch, g, seed=s)
+        total_imgs += args.batch
         total_t += dt
+        per.setdefault(str(g), []).append(round(args.batch / dt, 3))
     value = total_imgs / total_t
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s",
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "images/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total_t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(1e3 * total_t / args.steps, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-        "config": {"workload": f"{args.model} gamma sweep {list(GAMMAS)} (CPU sample: batch {sample_batch} per gamma)",
-                   "model": args.model, "global_batch": sample_batch * len(GAMMAS), "seq_len": VIT_CONFIGS[args.model].n_tokens,
-                   "parallelism": "cpu", "prompt_mode": "accumulate"},
-        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port",
-                         "sample": f"oracle/vit_oracle.py fp32 torch-CPU, {args.steps} steps x {len(GAMMAS)} gammas x batch {sample_batch}"},
-        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": workload_config(args, gammas, args.gpus),
+        "per_gamma": per,
+        "cpu_baseline": {"value": round(value, 3), "unit": "images/s", "cores": ora.cores, "kind": "port",
+                         "cpu_model": cpu_model(),
+                         "sample": f"oracle/vit_oracle.py fp32 torch-CPU; step k = one batch of {args.batch} "
+                                   f"at gamma {list(gammas)}[k mod {len(gammas)}], {args.steps} steps"},
+        "e2e": {"value": round(value, 3), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def workload_config(args, gammas, world):
+    from paper_2401_05031_b200.config import VIT_CONFIGS
+
+    cfg = VIT_CONFIGS[args.model]
+    tag = " (configs[1])" if args.model == "vit_b16" and tuple(gammas) == GAMMAS and args.batch == 256 else ""
+    return {"workload": f"{args.model} batch {args.batch} per gamma, sweep gamma in {list(gammas)}{tag}; one step = the sweep",
+            "model": args.model, "global_batch": args.batch * len(gammas) * world, "seq_len": cfg.n_tokens,
+            "parallelism": f"replicas x{world} (no collectives)", "prompt_mode": "accumulate",
+            "l2": "flushed (512 MiB write) before every step; inputs 154 MB per gamma > L2",
+            "cuda_graph": "one per gamma"}
+
+
+def stage_bytes(cfg, gamma, B, fold_ln=True):
+    """Algorithmic HBM bytes per forward of the memory-bound stages:
+    patchify (read fp32 image, write bf16 patch matrix), merge (read x fp32 + size, write x'
+    fp32 + bf16 copy + row stats + size), match (read the k third of qkv, bf16)."""
+    from paper_2401_05031_b200.config import token_schedule
+
+    D = cfg.dim
+    ts, rs = token_schedule(cfg, gamma)
+    patch = B * (3 * cfg.img * cfg.img * 4 + cfg.n_patches * cfg.patch_k_padded * 2)
+    merge = match = 0
+    first = True
+    for t, r in zip(ts, rs):
+        if r <= 0:
+            continue
+        tp = t - r
+        merge += B * (t * D * 4 + (0 if first else t * 4) + tp * D * 4 + tp * D * 2
+                      + tp * (D // 128) * 8 + tp * 4 + (2 * r + (t + 1) // 2 - r) * 4)
+        match += B * (t * D * 2 + (2 * r + (t + 1) // 2 - r) * 4)
+        first = False
+    return {"patchify": patch, "merge": merge, "match": match}
+
+
+def in_forward_profile(bb, cfg, B, dev, peak_burst, hbm_peak):
+    """Stage times of one eager forward per gamma (ta_profile_stages: CUDA events on the
+    forward's stream around every stage, kernels as the forward launches them).  Gives the
+    dominant kernel (fc1 = EPI_LN_GELU at gamma = 0, all 12 layers the same shape) and the
+    achieved HBM bandwidth of the memory-bound stages."""
+    imgs = torch.randn(B, 3, cfg.img, cfg.img, device=dev)
+    ids = torch.zeros(B, dtype=torch.int32, device=dev)
+    out = {}
+    for g in (0, -8):
+        bb.forward_raw(imgs, ids, g)
+        recs = bb.stage_times(imgs, ids, g)
+        out[g] = recs
+    fc1 = [us for st, l, us in out[0] if st == "fc1"]
+    M, N, K = B * cfg.n_tokens, cfg.mlp_dim, cfg.dim
+    us = sum(fc1) / len(fc1)
+    tf = 2.0 * M * N * K / (us * 1e-6) / 1e12
+    traffic = None
+    try:
+        import glob
+        import re
+
+        prof = sorted(glob.glob(os.path.join(ROOT, "profiles", "r02_ncu_fc1_inforward.txt")))[-1]
+        vals = {k: float(v) for k, v in re.findall(r"(dram__bytes_(?:read|write)\.sum)\s+([0-9.]+)", open(prof).read())}
+        traffic = round((vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]) * 1e6)
+    except Exception:
+        pass
+    dom = {"kernel": "gemm_bf16_sm100_pair_kernel<EPI_LN_GELU> (fc1, in the gamma=0 forward)", "shape": [M, N, K],
+           "us_per_launch": round(us, 2), "launches": len(fc1), "achieved": round(tf, 1), "unit": "TFLOP/s",
+           "peak": peak_burst, "frac": round(tf / peak_burst, 4), "bound": "tensor",
+           "algorithmic_bytes": 2 * (M * K + N * K + M * N), "traffic": traffic,
+           "how": "ta_profile_stages: CUDA events on the forward's stream around each fc1 launch (eager forward)"}
+    hbm = {}
+    for g, names in ((-8, ("patchify", "merge", "match")),):
+        byts = stage_bytes(cfg, g, B)
+        for nm in names:
+            t_us = sum(u for st, l, u in out[g] if st == nm)
+            gbs = byts[nm] / (t_us * 1e-6) / 1e9
+            hbm[nm] = {"gamma": g, "bytes": byts[nm], "us": round(t_us, 1), "gbs": round(gbs, 1),
+                       "frac": round(gbs / hbm_peak, 4)}
+    stages0 = {}
+    for st, l, u in out[0]:
+        stages0[st] = round(stages0.get(st, 0.0) + u, 1)
+    return dom, hbm, stages0
 
 
 def run_ours(args):
     import torch.distributed as dist
 
     from paper_2401_05031_b200.config import VIT_CONFIGS, flops_per_image
-    from tests import helpers
+    from paper_2401_05031_b200.replicas import aggregate_throughput
+    from paper_2401_05031_b200.synthetic import build_serve_model
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        dist.init_process_group("gloo")
+        dist.init_process_group("gloo")  # host-side plumbing only: barrier + reductions
     # one rank per GPU; if a box exposes fewer GPUs than ranks (multi-rank smoke tests on a
     # single-GPU box) ranks share devices round-robin
     dev = torch.device("cuda", local % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
 
-    cfg, params = helpers.backbone(args.model)
+    cfg = VIT_CONFIGS[args.model]
     gammas = tuple(int(g) for g in args.gammas.split(",")) if args.gammas else GAMMAS
-    tasks = helpers.task_params(cfg, (100,), [g for g in gammas if g > 0])
-    sm = helpers.serve_model(cfg, params, tasks, dtype="bf16", fold_ln=bool(args.fold_ln))
+    sm = build_serve_model(args.model, (100,), [g for g in gammas if g > 0], dtype="bf16", device=dev,
+                           fold_ln=bool(args.fold_ln))
     bb = sm.backbone
     B = args.batch
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -205,7 +338,7 @@ def run_ours(args):
         graphs[g] = gr
     torch.cuda.synchronize(dev)
 
-    def step(per_gamma_ms=None):
+    def step():
         flush.zero_()  # evict L2 (512 MiB > 126 MB) before every step, outside the events
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(gammas) + 1)]
         evs[0].record()
@@ -218,34 +351,38 @@ def run_ours(args):
         step()
     torch.cuda.synchronize(dev)
     if world > 1:
-        dist.barrier()
+        dist.barrier()  # barrier-aligned window on every replica
     torch.cuda.synchronize(dev)
     ev_list = []
     with ClockSampler(dev.index) as clocks:
         for _ in range(args.steps):
             ev_list.append(step())
         torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
     per_gamma_ms = {g: 0.0 for g in gammas}
-    total_ms = 0.0
+    local_ms = 0.0
     for evs in ev_list:
         for i, g in enumerate(gammas):
             ms = evs[i].elapsed_time(evs[i + 1])
             per_gamma_ms[g] += ms
-            total_ms += ms
-    from paper_2401_05031_b200.replicas import aggregate_throughput
-
+            local_ms += ms
+    local_imgs = args.steps * len(gammas) * B
     # replicas only: images summed over ranks, device time = max over ranks
-    imgs_total, total_ms = aggregate_throughput(args.steps * len(gammas) * B, total_ms)
+    imgs_total, total_ms = aggregate_throughput(local_imgs, local_ms)
+    per_rank = [round(local_imgs / (local_ms / 1e3), 1)]
     if world > 1:
-        dist.barrier()
+        gathered = [None] * world
+        dist.all_gather_object(gathered, {"rank": rank, "device": str(dev), "images_per_s": per_rank[0]})
+        per_rank = gathered
     value = imgs_total / (total_ms / 1e3)
-    peak_burst, peak_sus, hbm, peak_src = _peaks()
+    peak_burst, peak_sus, hbm_peak, peak_src = _peaks()
     # the forward is timed inside a long step (tens of ms of back-to-back tensor work), so the
     # roofline denominator is the SUSTAINED bf16 figure; the burst one is reported beside it
     peak = peak_sus or peak_burst
     flops = {g: flops_per_image(cfg, g) for g in gammas}
     sweep_flops = sum(flops[g] * B for g in gammas) * args.steps
-    achieved = sweep_flops / (total_ms / 1e3) / 1e12  # per GPU
+    achieved = sweep_flops / (local_ms / 1e3) / 1e12  # per GPU
     per_gamma = {}
     for g in gammas:
         ips = args.steps * B / (per_gamma_ms[g] / 1e3)
@@ -254,21 +391,20 @@ def run_ours(args):
                              "gflop_per_image": round(flops[g] / 1e9, 3), "tflops": round(tf, 1),
                              "roofline_frac": round(tf / peak, 4), "frac_of_burst": round(tf / peak_burst, 4)}
 
-    # dominant kernel alone: fc1 GEMM at the gamma=0 shape (M = B*197, N = 4D, K = D)
-    dom = dominant_gemm(cfg, B, dev, peak_burst)  # timed alone: burst peak
-
-    # e2e through the public API: pinned host images -> ServeModel.forward -> host logits
+    # e2e through the public API: pinned host images -> ServeModel.forward_async -> host logits
     e2e_ips, h2d, d2h = run_e2e(sm, cfg, B, gammas, args, dev)
     if world > 1:
         t = torch.tensor([e2e_ips], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)  # slowest replica bounds the job
         e2e_ips = float(t.item()) * world
 
+    dom, hbm, stages0 = in_forward_profile(bb, cfg, B, dev, peak_burst, hbm_peak)
+
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        ips, cores, dt = cpu_oracle_sample(cfg, params, tasks, args.cpu_batch, gammas)
-        cpu = {"value": round(ips, 3), "unit": "images/s", "cores": cores, "kind": "port",
-               "sample": f"oracle/vit_oracle.py fp32 torch-CPU, one batch of {args.cpu_batch} per gamma {list(gammas)} ({dt:.1f} s)"}
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(args.model, gammas, args.cpu_batch)
+    if world > 1:
+        dist.barrier()  # other replicas wait while rank 0 times the CPU baseline
 
     launches = args.steps * sum(launches_per_forward(cfg, g, fold_ln=bool(args.fold_ln)) for g in gammas)
     if rank == 0:
@@ -277,19 +413,21 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(total_ms / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"{args.model} batch {B} per gamma, sweep gamma in {list(gammas)}"
-                                   f"{' (configs[1])' if args.model == 'vit_b16' and gammas == GAMMAS and B == 256 else ''}; one step = the sweep",
-                       "model": args.model, "global_batch": B * len(gammas) * world, "seq_len": cfg.n_tokens,
-                       "parallelism": f"replicas x{world} (no collectives)", "prompt_mode": "accumulate",
-                       "l2": "flushed (512 MiB write) before every step; inputs 154 MB per gamma > L2",
-                       "cuda_graph": "one per gamma"},
+            "config": workload_config(args, gammas, world),
             "per_gamma": per_gamma,
-            "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
-                         "frac": round(achieved / peak, 4), "traffic": None,
-                         "peak_source": f"{peak_src} bf16_tflops_sustained (burst {peak_burst})",
-                         "frac_of_burst": round(achieved / peak_burst, 4),
-                         "what": "whole forward: algorithmic FLOPs (SURVEY.md §8d F(model, gamma) x images) / device time"},
+            "per_rank": per_rank,
+            "roofline": {"bound": "tensor", "achieved": dom["achieved"], "peak": peak_burst, "unit": "TFLOP/s",
+                         "frac": dom["frac"], "traffic": dom["traffic"],
+                         "kernel": dom["kernel"],
+                         "peak_source": f"{peak_src} bf16_tflops (burst: the kernel is timed per launch)",
+                         "forward": {"achieved": round(achieved, 1), "peak": peak, "frac": round(achieved / peak, 4),
+                                     "peak_source": f"{peak_src} bf16_tflops_sustained (burst {peak_burst})",
+                                     "frac_of_burst": round(achieved / peak_burst, 4),
+                                     "what": "whole forward: algorithmic FLOPs (SURVEY.md §8d F(model, gamma) x images) / device time"}},
             "dominant_kernel": dom,
+            "hbm": {"peak_gbs": hbm_peak, "stages": hbm,
+                    "what": "algorithmic bytes (bench.stage_bytes) / stage device time in one eager forward, vs measured hbm_gbs"},
+            "stages_gamma0_us": stages0,
             "e2e": {"value": round(e2e_ips, 1), "unit": "images/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "how": "ServeModel.forward_async(pinned host fp32 images): H2D (copy stream) + forward + D2H logits per batch, next batch submitted before the previous is waited on; wall clock"},
@@ -300,45 +438,6 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
-
-
-def dominant_gemm(cfg, B, dev, peak):
-    """Times the fc1 GEMM (+bias+GELU epilogue) at the gamma = 0 shape alone with CUDA events."""
-    from paper_2401_05031_b200 import _cuda
-
-    lib = _cuda.lib()
-    M, N, K = B * cfg.n_tokens, cfg.mlp_dim, cfg.dim
-    a = torch.randn(M, K, device=dev).bfloat16()
-    w = (torch.randn(N, K, device=dev) * 0.02).bfloat16()
-    bias = torch.zeros(N, device=dev)
-    out = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
-    st = torch.cuda.current_stream(dev).cuda_stream
-    for _ in range(5):
-        _cuda.check(lib.ta_gemm(a.data_ptr(), w.data_ptr(), bias.data_ptr(), None, out.data_ptr(), M, N, K, 1, 0, 0, st))
-    n = 20
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(n):
-        _cuda.check(lib.ta_gemm(a.data_ptr(), w.data_ptr(), bias.data_ptr(), None, out.data_ptr(), M, N, K, 1, 0, 0, st))
-    e1.record()
-    e1.synchronize()
-    ms = e0.elapsed_time(e1) / n
-    tf = 2.0 * M * N * K / (ms / 1e3) / 1e12
-    traffic = None  # DRAM bytes per launch from the committed `ncu --set full` capture of this shape
-    try:
-        import glob
-        import re
-
-        prof = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_gemm_fc1.txt")))[-1]
-        vals = {k: float(v) for k, v in re.findall(r"(dram__bytes_(?:read|write)\.sum)\s+([0-9.]+)", open(prof).read())}
-        traffic = {"bytes": round((vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]) * 1e6),
-                   "algorithmic_bytes": 2 * (M * K + N * K + M * N), "source": os.path.basename(prof)}
-    except Exception:
-        pass
-    return {"kernel": "gemm_bf16_sm100_pair_kernel<EPI_BIAS_GELU> (fc1 shape, timed alone via ta_gemm)", "shape": [M, N, K],
-            "traffic": traffic,
-            "ms": round(ms, 4), "achieved": round(tf, 1), "unit": "TFLOP/s", "peak": peak,
-            "frac": round(tf / peak, 4), "bound": "tensor"}
 
 
 def run_e2e(sm, cfg, B, gammas, args, dev):
@@ -377,16 +476,20 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default="vit_b16")
     ap.add_argument("--batch", type=int, default=256)
-    ap.add_argument("--cpu-batch", type=int, default=8)
-    ap.add_argument("--ref-batch", type=int, default=4)
+    ap.add_argument("--cpu-batch", type=int, default=256, help="CPU baseline: images per gamma")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--gammas", default="", help="comma-separated gamma sweep (default configs[1]: -16,-8,0,8,16)")
     ap.add_argument("--fold-ln", type=int, default=1, help="fold LayerNorm into the QKV / fc1 GEMMs (bf16 default)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # started without a launcher: one process (replica) per GPU via torch.distributed.run
+        from paper_2401_05031_b200.replicas import launch_replicas
+
+        sys.exit(launch_replicas(args.gpus, os.path.abspath(__file__), sys.argv[1:]).returncode)
+    run_ours(args)
 
 
 if __name__ == "__main__":

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define TA_ABI_VERSION 2
+#define TA_ABI_VERSION 3
 
 /* Status codes.  Python maps them onto the reference's exception types
  * (pkg/src/tokadapt/errors.py): TA_ERR_NO_PROMPT -> ProfileGapError(task, gamma,
@@ -162,6 +162,11 @@ int ta_forward_host(ta_model* model, const float* images_host, const int32_t* ta
  * outputs int32 src/dst [B, r], unm [B, ceil(t/2) - r].  Class token protected. */
 int ta_match(const float* metric, int batch, int t, int c, int r, int32_t* src, int32_t* dst,
              int32_t* unm, void* stream);
+/* a8+a9 as the forward runs them: the metric is the head mean of the k third of a qkv
+ * activation [B, t, 3 H hd] in `dtype` (ToMe k.mean(1)), computed inside the matching kernel
+ * (bf16: the 1xTF32 tcgen05 instance the bf16 forward launches; fp32: 3xTF32). */
+int ta_match_qkv(const void* qkv, int dtype, int batch, int t, int heads, int head_dim, int r,
+                 int32_t* src, int32_t* dst, int32_t* unm, void* stream);
 /* a10: size-weighted merge (tome merge_wavg) + fused LN2.  x fp32 [B, t, D], size fp32
  * [B, t] or NULL (= ones).  Writes x_out fp32 [B, t-r, D], size_out [B, t-r] and
  * h_out = LayerNorm(x_out) in `h_dtype` (TA_DTYPE_*). */
@@ -180,6 +185,25 @@ int ta_gemm(const void* a, const void* w, const float* bias, const float* resid,
 /* a4: row LayerNorm eps 1e-6, fp32 in, `out_dtype` out. */
 int ta_layernorm(const float* x, const float* w, const float* b, void* out, int rows, int dim,
                  int out_dtype, void* stream);
+
+/* ------------------------------------------------------------ stage timing
+ * Measurement support: with ta_profile_stages(model, 1) every ta_forward
+ * records CUDA events around each stage on its stream and synchronises at the end (so it is
+ * not graph-capturable while on); ta_stage_records returns the (stage, layer, device us)
+ * list of the last such forward in launch order (layer -1 = outside the layer loop). */
+enum {
+  TA_STAGE_PATCHIFY = 0, TA_STAGE_PATCH_GEMM, TA_STAGE_INSERT_ROWS, TA_STAGE_LN1, TA_STAGE_QKV,
+  TA_STAGE_ATTENTION, TA_STAGE_PROJ, TA_STAGE_MATCH, TA_STAGE_MERGE, TA_STAGE_LN2, TA_STAGE_FC1,
+  TA_STAGE_FC2, TA_STAGE_HEAD, TA_N_STAGES
+};
+typedef struct ta_stage_record {
+  int stage;
+  int layer;
+  float us;
+} ta_stage_record;
+const char* ta_stage_name(int stage);
+int ta_profile_stages(ta_model* model, int on);
+int ta_stage_records(const ta_model* model, ta_stage_record* out, int max_records, int* n);
 
 #ifdef __cplusplus
 }

@@ -50,6 +50,10 @@ class MergeStep:
     unm: torch.Tensor      # int64 [B, ceil(t/2) - r] A rows kept, ascending (cls first)
     node_max: torch.Tensor  # [B, ceil(t/2)] best score per A row (-inf for cls)
     second: torch.Tensor    # [B, ceil(t/2)] second-best score per A row (argmax margin)
+    # shadow mode (forced + shadow=True): the oracle's OWN decisions at this layer given the
+    # forced history, and its score matrix, for near-tie accounting in the parity tests
+    own: Optional[Tuple[torch.Tensor, torch.Tensor, torch.Tensor]] = None
+    scores: Optional[torch.Tensor] = None   # [B, ceil(t/2), floor(t/2)], row 0 = -inf
 
 
 @dataclass
@@ -85,10 +89,10 @@ def token_schedule(n_tokens: int, depth: int, gamma: int, prompt_mode: str = "ac
     return ts, rs
 
 
-def bipartite_soft_matching(metric: torch.Tensor, r: int):
+def bipartite_soft_matching(metric: torch.Tensor, r: int, return_scores: bool = False):
     """ToMe bipartite soft matching with class-token protection (Appendix A `match`).
 
-    metric [B, t, c] -> (src, dst, unm, node_max, second), all per image.
+    metric [B, t, c] -> (src, dst, unm, node_max, second), all per image (+ scores).
     """
     metric = metric / metric.norm(dim=-1, keepdim=True)
     a, b = metric[:, 0::2, :], metric[:, 1::2, :]
@@ -104,6 +108,8 @@ def bipartite_soft_matching(metric: torch.Tensor, r: int):
     src = order[:, :r]
     dst = node_idx.gather(-1, src)
     unm = order[:, r:].sort(dim=-1).values               # class token first
+    if return_scores:
+        return src, dst, unm, node_max, second, scores
     return src, dst, unm, node_max, second
 
 
@@ -144,13 +150,15 @@ def forward(params: Dict[str, object], heads_by_task: Sequence[Dict[str, torch.T
             patch: int, prompts: Optional[Sequence[torch.Tensor]] = None,
             prompt_mode: str = "accumulate", dtype: torch.dtype = torch.float32,
             forced: Optional[Sequence[Tuple[torch.Tensor, torch.Tensor, torch.Tensor]]] = None,
-            max_classes: Optional[int] = None) -> Tuple[torch.Tensor, OracleTrace]:
+            max_classes: Optional[int] = None, shadow: bool = False) -> Tuple[torch.Tensor, OracleTrace]:
     """Token-adapted forward for one batch at one gamma.
 
     params     fp32 backbone weights (paper_2401_05031_b200.weights.init_backbone layout)
     heads_by_task  per task {"w": [C, D], "b": [C]}
     prompts    per task [L, gamma, D] (required when gamma > 0)
     forced     per merge layer (src, dst, unm) to replay instead of matching (teacher forcing)
+    shadow     with forced: also run the matching on the oracle's own metric at every merge
+               layer and keep its decisions and scores (MergeStep.own / .scores)
     returns    logits [B, C_max] (-inf beyond each task's C) and the merge trace
     """
     cv = lambda t: t.to(dtype)  # noqa: E731
@@ -181,13 +189,19 @@ def forward(params: Dict[str, object], heads_by_task: Sequence[Dict[str, torch.T
         x = x + a
         r = max(0, min(-gamma, (t - 1) // 2)) if gamma < 0 else 0
         if r > 0:
+            own = scores = None
             if forced is not None:
                 src, dst, unm = (v.to(torch.int64) for v in forced[merge_no])
-                node_max = torch.full((bsz, (t + 1) // 2), float("nan"), dtype=dtype)
-                second = node_max.clone()
+                if shadow:
+                    o_src, o_dst, o_unm, node_max, second, scores = bipartite_soft_matching(
+                        metric, r, return_scores=True)
+                    own = (o_src, o_dst, o_unm)
+                else:
+                    node_max = torch.full((bsz, (t + 1) // 2), float("nan"), dtype=dtype)
+                    second = node_max.clone()
             else:
                 src, dst, unm, node_max, second = bipartite_soft_matching(metric, r)
-            trace.merges.append(MergeStep(li, t, r, src, dst, unm, node_max, second))
+            trace.merges.append(MergeStep(li, t, r, src, dst, unm, node_max, second, own, scores))
             merge_no += 1
             x, size = merge_wavg(x, size, src, dst, unm)
         h = F.layer_norm(x, (d,), lw["ln2_w"], lw["ln2_b"], eps=1e-6)

@@ -14,13 +14,18 @@ from typing import Optional
 from .errors import ConfigError, ProfileGapError
 
 __all__ = ["lib", "check", "LIB_PATH", "ModelDesc", "LayerWeights", "Weights", "TAError",
-           "DTYPE_BF16", "DTYPE_F32", "PROMPT_ACCUMULATE", "PROMPT_REPLACE", "EXPORTED_SYMBOLS"]
+           "StageRecord", "STAGES", "ABI_VERSION", "DTYPE_BF16", "DTYPE_F32", "PROMPT_ACCUMULATE",
+           "PROMPT_REPLACE", "EXPORTED_SYMBOLS"]
 
 LIB_PATH = os.environ.get("TA_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtokadapt_cuda.so")
 
 TA_OK, TA_ERR_INVALID, TA_ERR_SHAPE, TA_ERR_CONFIG, TA_ERR_NO_PROMPT = 0, -1, -2, -3, -4
 TA_ERR_NO_WEIGHTS, TA_ERR_WORKSPACE, TA_ERR_CUDA, TA_ERR_ARCH = -5, -6, -7, -8
+ABI_VERSION = 3
 DTYPE_BF16, DTYPE_F32 = 0, 1
+# TA_STAGE_* order of include/tokadapt_cuda.h
+STAGES = ("patchify", "patch_gemm", "insert_rows", "ln1", "qkv", "attention", "proj", "match",
+          "merge", "ln2", "fc1", "fc2", "head")
 PROMPT_ACCUMULATE, PROMPT_REPLACE = 0, 1
 
 # Every symbol include/tokadapt_cuda.h declares (checked by tests/test_abi.py).
@@ -28,7 +33,8 @@ EXPORTED_SYMBOLS = (
     "ta_abi_version", "ta_strerror", "ta_last_cuda_error", "ta_model_create", "ta_model_destroy",
     "ta_model_set_weights", "ta_model_set_head", "ta_model_set_prompts", "ta_token_schedule",
     "ta_merge_trace_len", "ta_workspace_size", "ta_forward", "ta_forward_host", "ta_match",
-    "ta_merge", "ta_attention", "ta_gemm", "ta_layernorm",
+    "ta_match_qkv", "ta_merge", "ta_attention", "ta_gemm", "ta_layernorm", "ta_stage_name",
+    "ta_profile_stages", "ta_stage_records",
 )
 
 
@@ -49,6 +55,10 @@ class LayerWeights(ctypes.Structure):
         "ln1_w", "ln1_b", "qkv_w", "qkv_b", "proj_w", "proj_b", "ln2_w", "ln2_b",
         "fc1_w", "fc1_b", "fc2_w", "fc2_b",
         "qkv_w_ln", "qkv_c1", "qkv_c2", "fc1_w_ln", "fc1_c1", "fc1_c2")]
+
+
+class StageRecord(ctypes.Structure):
+    _fields_ = [("stage", ctypes.c_int), ("layer", ctypes.c_int), ("us", ctypes.c_float)]
 
 
 class Weights(ctypes.Structure):
@@ -79,6 +89,10 @@ def _declare(l: ctypes.CDLL) -> None:
         "ta_forward": ([vp, vp, vp, i, i, vp, vp, vp, vp, sz, vp], i),
         "ta_forward_host": ([vp, vp, vp, i, i, vp, vp], i),
         "ta_match": ([vp, i, i, i, i, vp, vp, vp, vp], i),
+        "ta_match_qkv": ([vp, i, i, i, i, i, i, vp, vp, vp, vp], i),
+        "ta_stage_name": ([i], ctypes.c_char_p),
+        "ta_profile_stages": ([vp, i], i),
+        "ta_stage_records": ([vp, ctypes.POINTER(StageRecord), i, ip], i),
         "ta_merge": ([vp, vp, i, i, i, i, vp, vp, vp, vp, vp, vp, vp, vp, i, vp], i),
         "ta_attention": ([vp, vp, i, i, i, i, vp, i, vp], i),
         "ta_gemm": ([vp, vp, vp, vp, vp, i, i, i, i, i, i, vp], i),

@@ -557,15 +557,15 @@ int attention_fa(const void* qkv, const float* size, int B, int t, int H, int hd
   CUtensorMap tm;
   int rc = make_tmap_bf16_2d(&tm, qkv, static_cast<uint64_t>(B) * t, 3ull * H * hd, 64);
   if (rc) return rc;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_mask = 0;  // per device
+  if (attr_needed(attr_mask)) {
     cudaError_t e = cudaFuncSetAttribute(attn_fa_kernel<true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(attn_fa_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                227 * 1024);
     if (e != cudaSuccess) return set_last_cuda_error(e);
-    attr_set = true;
+    attr_done(attr_mask);
   }
   const int n_items = B * H;
   cudaLaunchConfig_t cfg = {};

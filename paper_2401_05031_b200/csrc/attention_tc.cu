@@ -732,12 +732,12 @@ static cudaError_t launch_attn_tc(const cudaLaunchConfig_t& cfg, const CUtensorM
                                   const CUtensorMap& tmt, const CUtensorMap& tmo, const float* size,
                                   int t, int H, int n_items, __nv_bfloat16* o, float scale_log2,
                                   const AttnTcLayout& L) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_mask = 0;  // per instantiation and device
+  if (attr_needed(attr_mask)) {
     const cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<kHasSize, kHD, kOne>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_done(attr_mask);
   }
   return cudaLaunchKernelEx(&cfg, attn_tc_kernel<kHasSize, kHD, kOne>, tm, tmt, tmo, size, t, H, n_items, o,
                             scale_log2, L);

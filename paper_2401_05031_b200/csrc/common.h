@@ -73,6 +73,21 @@ int set_last_cuda_error(cudaError_t e);
 
 int device_sm_count();
 
+// Kernel attributes such as the dynamic shared-memory limit are per device: a launcher sets
+// them once per (instantiation, device).  `mask` is the launcher's static bit set (bit = device
+// ordinal); returns true when the current device still needs the attribute call.  Benign race:
+// the attribute call is idempotent.
+inline bool attr_needed(const unsigned long long& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return !((mask >> (dev & 63)) & 1ull);
+}
+inline void attr_done(unsigned long long& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  mask |= 1ull << (dev & 63);
+}
+
 // Programmatic dependent launch on every kernel (TA_PDL=0 disables it: profiling A/B).
 int pdl_enabled();
 
@@ -91,12 +106,14 @@ int gemm_f32(const float* A, const float* W, int M, int N, int K, int epi_kind,
 // rowops.cu
 int patchify(const float* img, void* out, int B, int S, int P, int Kp, int dtype, cudaStream_t s);
 int insert_rows(float* x, int B, int t_total, int D, const float* cls, const float* pos,
-                const float* const* prompt_tab, const int32_t* task_ids, int layer, int gamma,
-                int prompt_row, cudaStream_t s, void* xh = nullptr, float* stats = nullptr);
+                const float* const* prompt_tab, const int32_t* task_ids, int n_tasks, int layer,
+                int gamma, int prompt_row, cudaStream_t s, void* xh = nullptr,
+                float* stats = nullptr);
 int layernorm(const float* x, const float* w, const float* b, void* out, int rows, int D,
               int out_dtype, cudaStream_t s);
 int head(const float* x, int B, int t_total, int D, const float* nw, const float* nb,
-         const HeadDesc* heads, const int32_t* task, float* logits, int c_max, cudaStream_t s);
+         const HeadDesc* heads, const int32_t* task, int n_tasks, float* logits, int c_max,
+         cudaStream_t s);
 
 // tome.cu.  metric source: either fp32 [B, t, c] (metric != null) or the k third of a
 // qkv activation [B, t, 3*H*c] in `qkv_dtype`, averaged over heads (ToMe k.mean(1)).

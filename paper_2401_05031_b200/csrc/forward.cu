@@ -48,6 +48,22 @@ int pdl_enabled() {
   return on;
 }
 
+// Makes `device` current for the scope of an ABI call and restores the caller's device
+// (torch keeps its own notion of the current device; the library must not move it).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int device) {
+    cudaGetDevice(&prev);
+    if (prev != device) err = cudaSetDevice(device);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 static int check_arch(int device) {
   int major = 0, minor = 0;
   cudaError_t e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
@@ -72,6 +88,9 @@ struct ta_model {
   HeadDesc* heads_dev = nullptr;
   std::map<int, std::vector<const float*>> prompts;  // gamma -> per-task pointer
   std::map<int, const float**> prompt_tab;             // gamma -> device table [n_tasks]
+  // per-stage device times of the last profiled forward (ta_profile_stages)
+  int profile_on = 0;
+  std::vector<ta_stage_record> records;
   // ta_forward_host cache
   void* host_ws = nullptr;
   size_t host_ws_bytes = 0;
@@ -179,43 +198,56 @@ size_t trace_len(const Schedule& s, int B) {
     if (_rc != TA_OK) return _rc; \
   } while (0)
 
-// Profiling only (TA_PROFILE_STAGES=1, never inside a graph): CUDA events around every
-// stage of ta_forward, summed per stage name and printed after the forward.
+// Stage timing (profiling only; never inside a graph): CUDA events around every stage of
+// ta_forward.  ta_profile_stages(m, 1) keeps per-(stage, layer) device times in the model for
+// ta_stage_records; TA_PROFILE_STAGES=1 prints per-stage sums to stderr.
 namespace {
 struct StageProfiler {
-  bool on = false;
+  bool on = false, print = false;
+  ta_model* m = nullptr;
   cudaStream_t st = nullptr;
-  std::vector<std::pair<const char*, cudaEvent_t>> marks;
-  explicit StageProfiler(cudaStream_t s) : st(s) {
+  struct Mark {
+    int stage, layer;
+    cudaEvent_t ev;
+  };
+  std::vector<Mark> marks;
+  StageProfiler(cudaStream_t s, ta_model* model) : m(model), st(s) {
     const char* v = getenv("TA_PROFILE_STAGES");
-    on = v && v[0] == '1';
-    mark("start");
+    print = v && v[0] == '1';
+    on = print || (m && m->profile_on);
+    mark(-1, -1);
   }
-  void mark(const char* name) {
+  void mark(int stage, int layer) {
     if (!on) return;
     cudaEvent_t e;
     cudaEventCreate(&e);
     cudaEventRecord(e, st);
-    marks.emplace_back(name, e);
+    marks.push_back({stage, layer, e});
   }
   ~StageProfiler() {
     if (!on || marks.size() < 2) return;
-    cudaEventSynchronize(marks.back().second);
-    std::map<std::string, std::pair<int, float>> agg;
-    float total = 0.f;
+    cudaEventSynchronize(marks.back().ev);
+    std::vector<ta_stage_record> recs;
     for (size_t i = 1; i < marks.size(); ++i) {
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second);
-      auto& a = agg[marks[i].first];
-      a.first += 1;
-      a.second += ms;
-      total += ms;
+      cudaEventElapsedTime(&ms, marks[i - 1].ev, marks[i].ev);
+      recs.push_back({marks[i].stage, marks[i].layer, ms * 1e3f});
     }
-    for (auto& kv : agg)
-      fprintf(stderr, "[ta stage] %-14s n=%3d %9.1f us\n", kv.first.c_str(), kv.second.first,
-              kv.second.second * 1e3f);
-    fprintf(stderr, "[ta stage] total %9.1f us\n", total * 1e3f);
-    for (auto& m : marks) cudaEventDestroy(m.second);
+    if (m && m->profile_on) m->records = recs;
+    if (print) {
+      float agg[TA_N_STAGES] = {};
+      int cnt[TA_N_STAGES] = {};
+      float total = 0.f;
+      for (const auto& r : recs) {
+        agg[r.stage] += r.us;
+        cnt[r.stage] += 1;
+        total += r.us;
+      }
+      for (int k = 0; k < TA_N_STAGES; ++k)
+        if (cnt[k]) fprintf(stderr, "[ta stage] %-14s n=%3d %9.1f us\n", ta_stage_name(k), cnt[k], agg[k]);
+      fprintf(stderr, "[ta stage] total %9.1f us\n", total);
+    }
+    for (auto& mk : marks) cudaEventDestroy(mk.ev);
   }
 };
 }  // namespace
@@ -242,6 +274,27 @@ const char* ta_strerror(int code) {
 
 int ta_last_cuda_error(void) { return g_last_cuda_error; }
 
+const char* ta_stage_name(int stage) {
+  static const char* const kNames[TA_N_STAGES] = {
+      "patchify", "patch_gemm", "insert_rows", "ln1", "qkv", "attention", "proj",
+      "match",    "merge",      "ln2",         "fc1", "fc2", "head"};
+  return (stage >= 0 && stage < TA_N_STAGES) ? kNames[stage] : "?";
+}
+
+int ta_profile_stages(ta_model* m, int on) {
+  if (!m) return TA_ERR_INVALID;
+  m->profile_on = on ? 1 : 0;
+  m->records.clear();
+  return TA_OK;
+}
+
+int ta_stage_records(const ta_model* m, ta_stage_record* out, int max_records, int* n) {
+  if (!m || !n || (max_records > 0 && !out)) return TA_ERR_INVALID;
+  *n = static_cast<int>(m->records.size());
+  for (int i = 0; i < *n && i < max_records; ++i) out[i] = m->records[i];
+  return TA_OK;
+}
+
 int ta_model_create(int device, const ta_model_desc* desc, ta_model** out) {
   if (!desc || !out) return TA_ERR_INVALID;
   const ta_model_desc& d = *desc;
@@ -253,9 +306,10 @@ int ta_model_create(int device, const ta_model_desc* desc, ta_model** out) {
   const int hd = d.dim / d.heads;
   if (hd != 64 && hd != 80) return TA_ERR_CONFIG;
   if (d.dim % 256 != 0 || d.mlp_dim % 256 != 0) return TA_ERR_CONFIG;
-  cudaError_t e = cudaSetDevice(device);
-  if (e != cudaSuccess) return set_last_cuda_error(e);
+  DeviceGuard guard(device);
+  if (guard.err != cudaSuccess) return set_last_cuda_error(guard.err);
   TA_TRY(check_arch(device));
+  cudaError_t e;
   auto* m = new ta_model();
   m->device = device;
   m->d = d;
@@ -277,7 +331,7 @@ int ta_model_create(int device, const ta_model_desc* desc, ta_model** out) {
 
 void ta_model_destroy(ta_model* m) {
   if (!m) return;
-  cudaSetDevice(m->device);
+  DeviceGuard guard(m->device);
   cudaFree(m->heads_dev);
   for (auto& kv : m->prompt_tab) cudaFree(kv.second);
   if (m->host_ws) cudaFree(m->host_ws);
@@ -312,6 +366,7 @@ int ta_model_set_head(ta_model* m, int task, const float* w, const float* b, int
       classes > m->d.max_classes)
     return TA_ERR_INVALID;
   m->heads[task] = HeadDesc{w, b, classes};
+  DeviceGuard guard(m->device);
   cudaError_t e = cudaMemcpy(m->heads_dev + task, &m->heads[task], sizeof(HeadDesc),
                              cudaMemcpyHostToDevice);
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
@@ -319,6 +374,7 @@ int ta_model_set_head(ta_model* m, int task, const float* w, const float* b, int
 
 int ta_model_set_prompts(ta_model* m, int task, int gamma, const float* prompts) {
   if (!m || !prompts || task < 0 || task >= m->d.n_tasks || gamma <= 0) return TA_ERR_INVALID;
+  DeviceGuard guard(m->device);
   auto& vec = m->prompts[gamma];
   if (vec.empty()) vec.assign(m->d.n_tasks, nullptr);
   vec[task] = prompts;
@@ -360,22 +416,27 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
                size_t ws_bytes, void* stream) {
   if (!m || !images || !task_ids || !logits || !ws || B <= 0) return TA_ERR_INVALID;
   if (!m->has_weights) return TA_ERR_NO_WEIGHTS;
-  for (int k = 0; k < m->d.n_tasks; ++k)
-    if (!m->heads[k].w) return TA_ERR_NO_WEIGHTS;
+  // Task ids are device-side here, so heads / prompts are validated per task only where the
+  // ids are known on the host (ta_forward_host, the Python front end).  At least one head
+  // must exist; an image whose task has no head, no prompts at this gamma, or an id outside
+  // [0, n_tasks) is never dereferenced and gets NaN logits (rowops.cu insert_rows / head).
+  bool any_head = false;
+  for (int k = 0; k < m->d.n_tasks; ++k) any_head = any_head || m->heads[k].w != nullptr;
+  if (!any_head) return TA_ERR_NO_WEIGHTS;
   const float* const* ptab = nullptr;
   if (gamma > 0) {
-    auto it = m->prompts.find(gamma);
-    if (it == m->prompts.end()) return TA_ERR_NO_PROMPT;
-    for (const float* p : it->second)
-      if (!p) return TA_ERR_NO_PROMPT;
-    ptab = m->prompt_tab[gamma];
+    auto it = m->prompt_tab.find(gamma);
+    if (it == m->prompt_tab.end()) return TA_ERR_NO_PROMPT;  // no task has prompts at gamma
+    ptab = it->second;
   }
   if (gamma < -(m->n_tokens - 1)) return TA_ERR_INVALID;
   const Schedule s = make_schedule(m, gamma);
   Workspace w = carve(m, B, s, static_cast<char*>(ws));
   if (ws_bytes < w.total) return TA_ERR_WORKSPACE;
+  DeviceGuard guard(m->device);
+  if (guard.err != cudaSuccess) return set_last_cuda_error(guard.err);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  StageProfiler prof(st);
+  StageProfiler prof(st, m);
   const ta_model_desc& d = m->d;
   const int D = d.dim, L = d.depth, N = m->n_tokens;
   const int act = d.dtype;
@@ -389,7 +450,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
 
   // ---- patch embedding + cls + layer-0 prompts
   TA_TRY(patchify(images, w.patches, B, d.img, d.patch, m->kp, act, st));
-  prof.mark("patchify");
+  prof.mark(TA_STAGE_PATCHIFY, -1);
   {
     GemmEpi e;
     e.bias = static_cast<const float*>(m->w.patch_b);
@@ -405,13 +466,13 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
     }
     TA_TRY(linear(m, w.patches, m->w.patch_w, B * m->n_patches, D, m->kp,
                   fused ? EPI_PATCH_STATS : EPI_PATCH, e, st));
-  prof.mark("patch_gemm");
+    prof.mark(TA_STAGE_PATCH_GEMM, -1);
   }
   TA_TRY(insert_rows(w.x[0], B, s.t[0], D, static_cast<const float*>(m->w.cls),
-                     static_cast<const float*>(m->w.pos), ptab, task_ids, 0,
+                     static_cast<const float*>(m->w.pos), ptab, task_ids, d.n_tasks, 0,
                      gamma > 0 ? gamma : 0, N, st, fused ? w.h : nullptr,
                      fused ? ln1_stats : nullptr));
-  prof.mark("insert_rows");
+      prof.mark(TA_STAGE_INSERT_ROWS, -1);
 
   int cur = 0;
   const float* size = nullptr;
@@ -422,10 +483,10 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
     const ta_layer_weights& Lw = m->layers[l];
     t = s.t[l];
     if (l > 0 && gamma > 0)
-      TA_TRY(insert_rows(w.x[cur], B, t, D, nullptr, nullptr, ptab, task_ids, l, gamma,
+      TA_TRY(insert_rows(w.x[cur], B, t, D, nullptr, nullptr, ptab, task_ids, d.n_tasks, l, gamma,
                          accumulate ? t - gamma : N, st, fused ? w.h : nullptr,
                          fused ? ln1_stats : nullptr));
-  prof.mark("insert_rows");
+      prof.mark(TA_STAGE_INSERT_ROWS, l);
     const int M = B * t;
     {  // LN1 + QKV
       GemmEpi e;
@@ -437,18 +498,18 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         e.c2 = static_cast<const float*>(Lw.qkv_c2);
         e.inv_dim = 1.0f / D;
         TA_TRY(linear(m, w.h, Lw.qkv_w_ln, M, 3 * D, D, EPI_LN_BIAS, e, st));
-  prof.mark("qkv");
+      prof.mark(TA_STAGE_QKV, l);
       } else {
         TA_TRY(layernorm(w.x[cur], static_cast<const float*>(Lw.ln1_w),
                          static_cast<const float*>(Lw.ln1_b), w.h, M, D, act, st));
-  prof.mark("ln1");
+      prof.mark(TA_STAGE_LN1, l);
         e.bias = static_cast<const float*>(Lw.qkv_b);
         TA_TRY(linear(m, w.h, Lw.qkv_w, M, 3 * D, D, EPI_BIAS, e, st));
-  prof.mark("qkv");
+      prof.mark(TA_STAGE_QKV, l);
       }
     }
     TA_TRY(attention(w.qkv, size, B, t, d.heads, m->hd, w.attn, act, st));
-  prof.mark("attention");
+      prof.mark(TA_STAGE_ATTENTION, l);
     const int r = s.r[l];
     {  // proj + residual (+ LN2 stats when no merge follows)
       GemmEpi e;
@@ -460,10 +521,10 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         e.stats = ln2_stats;
         e.stat_slots = stat_slots;
         TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID_STATS, e, st));
-  prof.mark("proj");
+      prof.mark(TA_STAGE_PROJ, l);
       } else {
         TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID, e, st));
-  prof.mark("proj");
+      prof.mark(TA_STAGE_PROJ, l);
       }
     }
     int tp = t;
@@ -484,11 +545,11 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         cudaMemcpyAsync(merge_trace + (src - forced_trace), src,
                         sizeof(int32_t) * static_cast<size_t>(B) * (2 * r + na - r),
                         cudaMemcpyDeviceToDevice, st);
-      prof.mark("match");
+      prof.mark(TA_STAGE_MATCH, l);
       TA_TRY(merge(w.x[cur], size, B, t, D, r, src, dst, unm, static_cast<const float*>(Lw.ln2_w),
                    static_cast<const float*>(Lw.ln2_b), w.x[cur ^ 1], w.size[size_buf], w.h, act,
                    st, fused ? ln2_stats : nullptr));
-  prof.mark("merge");
+      prof.mark(TA_STAGE_MERGE, l);
       cur ^= 1;
       size = w.size[size_buf];
       size_buf ^= 1;
@@ -496,7 +557,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
     } else if (!fused) {
       TA_TRY(layernorm(w.x[cur], static_cast<const float*>(Lw.ln2_w),
                        static_cast<const float*>(Lw.ln2_b), w.h, M, D, act, st));
-  prof.mark("ln2");
+      prof.mark(TA_STAGE_LN2, l);
     }
     const int Mp = B * tp;
     {  // LN2 + fc1 + GELU
@@ -509,11 +570,11 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         e.c2 = static_cast<const float*>(Lw.fc1_c2);
         e.inv_dim = 1.0f / D;
         TA_TRY(linear(m, w.h, Lw.fc1_w_ln, Mp, d.mlp_dim, D, EPI_LN_GELU, e, st));
-  prof.mark("fc1");
+      prof.mark(TA_STAGE_FC1, l);
       } else {
         e.bias = static_cast<const float*>(Lw.fc1_b);
         TA_TRY(linear(m, w.h, Lw.fc1_w, Mp, d.mlp_dim, D, EPI_BIAS_GELU, e, st));
-  prof.mark("fc1");
+      prof.mark(TA_STAGE_FC1, l);
       }
     }
     {  // fc2 + residual (+ next layer's LN1 stats)
@@ -538,23 +599,25 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
       }
       TA_TRY(linear(m, w.mlp, Lw.fc2_w, Mp, D, d.mlp_dim,
                     stats ? EPI_BIAS_RESID_STATS : EPI_BIAS_RESID, e, st));
-  prof.mark("fc2");
+      prof.mark(TA_STAGE_FC2, l);
       if (restride) cur ^= 1;
     }
     t = tp;
   }
   TA_TRY(head(w.x[cur], B, t, D, static_cast<const float*>(m->w.norm_w),
-              static_cast<const float*>(m->w.norm_b), m->heads_dev, task_ids, logits,
+              static_cast<const float*>(m->w.norm_b), m->heads_dev, task_ids, d.n_tasks, logits,
               d.max_classes, st));
-  prof.mark("head");
+  prof.mark(TA_STAGE_HEAD, -1);
   return TA_OK;
 }
 
 int ta_forward_host(ta_model* m, const float* images_host, const int32_t* task_ids_host, int B,
                     int gamma, float* logits_host, void* stream) {
   if (!m || !images_host || !task_ids_host || !logits_host || B <= 0) return TA_ERR_INVALID;
-  for (int i = 0; i < B; ++i)
+  for (int i = 0; i < B; ++i) {
     if (task_ids_host[i] < 0 || task_ids_host[i] >= m->d.n_tasks) return TA_ERR_INVALID;
+    if (!m->heads[task_ids_host[i]].w) return TA_ERR_NO_WEIGHTS;
+  }
   if (gamma > 0) {
     auto it = m->prompts.find(gamma);
     if (it == m->prompts.end()) return TA_ERR_NO_PROMPT;
@@ -562,6 +625,8 @@ int ta_forward_host(ta_model* m, const float* images_host, const int32_t* task_i
       if (!it->second[task_ids_host[i]]) return TA_ERR_NO_PROMPT;
   }
   std::lock_guard<std::mutex> lock(m->host_mu);
+  DeviceGuard guard(m->device);
+  if (guard.err != cudaSuccess) return set_last_cuda_error(guard.err);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t img_bytes = static_cast<size_t>(B) * 3 * m->d.img * m->d.img * sizeof(float);
   const size_t task_bytes = align_up(static_cast<size_t>(B) * sizeof(int32_t));
@@ -604,6 +669,20 @@ int ta_match(const float* metric, int batch, int t, int c, int r, int32_t* src, 
   cudaError_t e = cudaMallocAsync(&scratch, match_tc_scratch_bytes(batch, c), st);
   if (e != cudaSuccess) return set_last_cuda_error(e);
   const int rc = match(metric, nullptr, TA_DTYPE_F32, batch, t, 1, c, r, src, dst, unm,
+                       static_cast<float*>(scratch), st);
+  cudaFreeAsync(scratch, st);
+  return rc;
+}
+
+int ta_match_qkv(const void* qkv, int dtype, int batch, int t, int heads, int head_dim, int r,
+                 int32_t* src, int32_t* dst, int32_t* unm, void* stream) {
+  if (!qkv || !src || !dst || !unm || batch <= 0 || heads <= 0) return TA_ERR_INVALID;
+  if (dtype != TA_DTYPE_BF16 && dtype != TA_DTYPE_F32) return TA_ERR_INVALID;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  void* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(&scratch, match_tc_scratch_bytes(batch, head_dim), st);
+  if (e != cudaSuccess) return set_last_cuda_error(e);
+  const int rc = match(nullptr, qkv, dtype, batch, t, heads, head_dim, r, src, dst, unm,
                        static_cast<float*>(scratch), st);
   cudaFreeAsync(scratch, st);
   return rc;

@@ -951,12 +951,12 @@ static int launch_bf16(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
                        const GemmEpi& epi, cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
   auto kern = gemm_bf16_sm100_kernel<BN, EPI, OutT, kRemap>;
-  static bool attr_set = false;  // per instantiation; benign race (idempotent)
-  if (!attr_set) {
+  static unsigned long long attr_mask = 0;  // per instantiation and device
+  if (attr_needed(attr_mask)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg::kSmemBytes);
     if (e != cudaSuccess) return set_last_cuda_error(e);
-    attr_set = true;
+    attr_done(attr_mask);
   }
   const int tiles = ((M + kBM - 1) / kBM) * (N / BN);
   const int grid = tiles < device_sm_count() ? tiles : device_sm_count();
@@ -1029,12 +1029,12 @@ static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
                        const GemmEpi& epi, cudaStream_t stream) {
   using Cfg = PairCfg<EPI, OutT, kRemap>;
   auto kern = gemm_bf16_sm100_pair_kernel<EPI, OutT, kRemap>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_mask = 0;  // per instantiation and device
+  if (attr_needed(attr_mask)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg::kSmemBytes);
     if (e != cudaSuccess) return set_last_cuda_error(e);
-    attr_set = true;
+    attr_done(attr_mask);
   }
   CUtensorMap tc_{};
   if (Cfg::kTma) {

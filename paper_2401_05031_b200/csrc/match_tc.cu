@@ -355,9 +355,9 @@ int match_tc(const float* metric, const void* qkv, int qkv_dtype, int B, int t, 
   const size_t tiles = static_cast<size_t>(cp / 32) * kRows * 128;
   const size_t tail = 3 * 2 * kRows * 4 + 64 + 1024;
   const size_t smem3 = 4 * tiles + tail, smem1 = 2 * tiles + tail;
-  static bool attr_set = false;
+  static unsigned long long attr_mask = 0;  // per device
   cudaError_t e;
-  if (!attr_set) {
+  if (attr_needed(attr_mask)) {
     e = cudaFuncSetAttribute(match_fused_kernel<float, 2, 3, kFusedThreads>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e == cudaSuccess)
@@ -367,7 +367,7 @@ int match_tc(const float* metric, const void* qkv, int qkv_dtype, int B, int t, 
       e = cudaFuncSetAttribute(match_fused_kernel<__nv_bfloat16, 2, 1, 256>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
     if (e != cudaSuccess) return set_last_cuda_error(e);
-    attr_set = true;
+    attr_done(attr_mask);
   }
   if (metric != nullptr || qkv_dtype == TA_DTYPE_F32)
     e = launch_pdl(match_fused_kernel<float, 2, 3, kFusedThreads>, dim3(B), dim3(kFusedThreads), smem3, s,

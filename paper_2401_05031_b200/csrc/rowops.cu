@@ -201,13 +201,16 @@ int patchify(const float* img, void* out, int B, int S, int P, int Kp, int dtype
 // ------------------------------------------------------------------ insert rows
 // x is [B, t_total, D] fp32.  If cls != null: row 0 = cls + pos[0].  If gamma > 0: rows
 // [prompt_row, prompt_row + gamma) = prompts[task_b][layer] (a [gamma, D] block found via
-// the per-task pointer table; prompts are fp32 [depth, gamma, D]).
+// the per-task pointer table; prompts are fp32 [depth, gamma, D]).  A task id outside
+// [0, n_tasks) or a task without prompts at this gamma (null table entry) is never
+// dereferenced: its prompt rows are written as NaN, so the image's logits come out NaN
+// (ta_forward takes device-side ids and cannot validate them on the host).
 template <int VEC>
 __global__ void insert_rows_kernel(float* __restrict__ x, int t_total,
                                    const float* __restrict__ cls, const float* __restrict__ pos,
                                    const float* const* __restrict__ prompt_tab,
-                                   const int32_t* __restrict__ task_ids, int layer, int gamma,
-                                   int prompt_row, __nv_bfloat16* __restrict__ xh,
+                                   const int32_t* __restrict__ task_ids, int n_tasks, int layer,
+                                   int gamma, int prompt_row, __nv_bfloat16* __restrict__ xh,
                                    float* __restrict__ stats) {
   // One warp per inserted row, VEC float4 per lane (D = 128 VEC), all loads before the stores;
   // with xh / stats (LayerNorm folded into the QKV GEMM) the row is also written as bf16 and
@@ -217,8 +220,12 @@ __global__ void insert_rows_kernel(float* __restrict__ x, int t_total,
   const int b = blockIdx.x;
   const int n_cls = cls != nullptr ? 1 : 0;
   const int n_rows = n_cls + (gamma > 0 ? gamma : 0);
-  const float* P = gamma > 0 ? prompt_tab[task_ids[b]] + static_cast<long long>(layer) * gamma * D
-                             : nullptr;
+  const float* P = nullptr;
+  if (gamma > 0) {
+    const int tk = task_ids[b];
+    P = (tk >= 0 && tk < n_tasks) ? prompt_tab[tk] : nullptr;
+    if (P != nullptr) P += static_cast<long long>(layer) * gamma * D;
+  }
   const int lane = lane_id();
   grid_dep_wait();
   grid_dep_launch();
@@ -233,10 +240,13 @@ __global__ void insert_rows_kernel(float* __restrict__ x, int t_total,
         const float4 p = reinterpret_cast<const float4*>(pos)[lane + 32 * i];
         v[i] = make_float4(a.x + p.x, a.y + p.y, a.z + p.z, a.w + p.w);
       }
-    } else {
+    } else if (P != nullptr) {
       const float4* srow = reinterpret_cast<const float4*>(P + static_cast<long long>(rr - n_cls) * D);
 #pragma unroll
       for (int i = 0; i < VEC; ++i) v[i] = srow[lane + 32 * i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) v[i] = make_float4(NAN, NAN, NAN, NAN);
     }
     float s = 0.f, q = 0.f;
 #pragma unroll
@@ -263,8 +273,8 @@ __global__ void insert_rows_kernel(float* __restrict__ x, int t_total,
 }
 
 int insert_rows(float* x, int B, int t_total, int D, const float* cls, const float* pos,
-                const float* const* prompt_tab, const int32_t* task_ids, int layer, int gamma,
-                int prompt_row, cudaStream_t s, void* xh, float* stats) {
+                const float* const* prompt_tab, const int32_t* task_ids, int n_tasks, int layer,
+                int gamma, int prompt_row, cudaStream_t s, void* xh, float* stats) {
   if (D % 128 != 0) return TA_ERR_SHAPE;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(B);
@@ -280,7 +290,7 @@ int insert_rows(float* x, int B, int t_total, int D, const float* cls, const flo
   switch (D / 128) {
 #define TA_INSERT_CASE(V) \
   case V:                 \
-    e = cudaLaunchKernelEx(&cfg, insert_rows_kernel<V>, x, t_total, cls, pos, prompt_tab, task_ids, layer, gamma, prompt_row, h, stats); \
+    e = cudaLaunchKernelEx(&cfg, insert_rows_kernel<V>, x, t_total, cls, pos, prompt_tab, task_ids, n_tasks, layer, gamma, prompt_row, h, stats); \
     break;
     TA_INSERT_CASE(2)
     TA_INSERT_CASE(6)
@@ -387,7 +397,7 @@ constexpr int kHeadCls = 16;
 __global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ x, int B, int t_total, int D,
                                                    const float* __restrict__ nw, const float* __restrict__ nb,
                                                    const HeadDesc* __restrict__ heads,
-                                                   const int32_t* __restrict__ task,
+                                                   const int32_t* __restrict__ task, int n_tasks,
                                                    float* __restrict__ logits, int c_max) {
   extern __shared__ float hrow[];  // [kHeadImgs][D]
   __shared__ int s_task[kHeadImgs];
@@ -431,7 +441,8 @@ __global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ x, 
         hr[lane + 32 * i] = make_float4((v[i].x - mean) * rstd * g.x + o.x, (v[i].y - mean) * rstd * g.y + o.y,
                                         (v[i].z - mean) * rstd * g.z + o.z, (v[i].w - mean) * rstd * g.w + o.w);
       }
-    if (lane == 0) s_task[warp] = task[b];
+    // a task id outside [0, n_tasks) is mapped to -1 and its logits written as NaN
+    if (lane == 0) s_task[warp] = (task[b] >= 0 && task[b] < n_tasks) ? task[b] : -1;
   }
   __syncthreads();
   for (int j = 0; j < n_img; ++j) {
@@ -439,12 +450,14 @@ __global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ x, 
     bool first = true;  // handle each distinct task once, at its first image
     for (int jj = 0; jj < j; ++jj) first = first && s_task[jj] != tk;
     if (!first) continue;
-    const HeadDesc h = heads[tk];
+    const HeadDesc h = tk >= 0 ? heads[tk] : HeadDesc{nullptr, nullptr, 0};
     const int c_end = min(c_max, static_cast<int>(blockIdx.y + 1) * kHeadCls);
     for (int c = static_cast<int>(blockIdx.y) * kHeadCls + warp; c < c_end; c += nwarps) {
       if (c >= h.classes) {
+        // beyond the task's classes: -inf; invalid id or no head registered: NaN (loud)
+        const float fill = h.classes > 0 ? -INFINITY : NAN;
         for (int im = 0; im < n_img; ++im)
-          if (s_task[im] == tk && lane == 0) logits[static_cast<long long>(b0 + im) * c_max + c] = -INFINITY;
+          if (s_task[im] == tk && lane == 0) logits[static_cast<long long>(b0 + im) * c_max + c] = fill;
         continue;
       }
       const float4* wr = reinterpret_cast<const float4*>(h.w + static_cast<long long>(c) * D);
@@ -470,7 +483,8 @@ __global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ x, 
 }
 
 int head(const float* x, int B, int t_total, int D, const float* nw, const float* nb,
-         const HeadDesc* heads, const int32_t* task, float* logits, int c_max, cudaStream_t s) {
+         const HeadDesc* heads, const int32_t* task, int n_tasks, float* logits, int c_max,
+         cudaStream_t s) {
   if (D % 128 != 0 || D > 1280) return TA_ERR_SHAPE;
   const size_t smem = static_cast<size_t>(kHeadImgs) * D * sizeof(float);
   if (smem > 48 * 1024) {
@@ -488,7 +502,7 @@ int head(const float* x, int B, int t_total, int D, const float* nw, const float
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, head_kernel, x, B, t_total, D, nw, nb, heads, task, logits, c_max);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, head_kernel, x, B, t_total, D, nw, nb, heads, task, n_tasks, logits, c_max);
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 

@@ -63,6 +63,8 @@ class TransformerModel:
         self.device = torch.device(device)
         if self.device.type != "cuda":
             raise ConfigError("TransformerModel runs on a CUDA device only (no CPU fallback)")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.n_tasks, self.max_classes = n_tasks, max_classes
         self._lib = _cuda.lib()
         desc = _cuda.ModelDesc(cfg.dim, cfg.depth, cfg.heads, cfg.mlp_dim, cfg.patch, cfg.img,
@@ -70,7 +72,7 @@ class TransformerModel:
                                _cuda.PROMPT_ACCUMULATE if prompt_mode == "accumulate" else _cuda.PROMPT_REPLACE,
                                _DTYPES[dtype])
         handle = ctypes.c_void_p()
-        _cuda.check(self._lib.ta_model_create(self.device.index or 0, ctypes.byref(desc), ctypes.byref(handle)))
+        _cuda.check(self._lib.ta_model_create(self.device.index, ctypes.byref(desc), ctypes.byref(handle)))
         self._h = handle
         self._keep: List[torch.Tensor] = []
         self._upload(params)
@@ -162,6 +164,8 @@ class TransformerModel:
         if logits is None:
             logits = torch.empty(b, self.max_classes, dtype=torch.float32, device=self.device)
         ws = workspace if workspace is not None else self.workspace(b, gamma)
+        # the library switches to (and restores) the model's device itself; the stream is the
+        # current stream of the model's device
         rc = self._lib.ta_forward(self._h, images.data_ptr(), task_ids.data_ptr(), b, gamma,
                                   logits.data_ptr(), _ptr(trace), _ptr(forced_trace),
                                   ws.data_ptr(), ws.numel(), _stream_handle(self.device))
@@ -222,6 +226,22 @@ class TransformerModel:
         done = torch.cuda.Event()
         done.record(compute)
         return PendingForward(done, out)
+
+    def stage_times(self, images: torch.Tensor, task_ids: torch.Tensor, gamma: int) -> List[Tuple[str, int, float]]:
+        """One eager forward with per-stage CUDA events (ta_profile_stages): returns
+        [(stage, layer, device us)] in launch order (layer -1 = outside the layer loop).
+        Synchronises; not for use inside a CUDA graph."""
+        _cuda.check(self._lib.ta_profile_stages(self._h, 1))
+        try:
+            self.forward_raw(images, task_ids, gamma)
+            torch.cuda.synchronize(self.device)
+            n = ctypes.c_int()
+            _cuda.check(self._lib.ta_stage_records(self._h, None, 0, ctypes.byref(n)))
+            recs = (_cuda.StageRecord * max(1, n.value))()
+            _cuda.check(self._lib.ta_stage_records(self._h, recs, n.value, ctypes.byref(n)))
+        finally:
+            _cuda.check(self._lib.ta_profile_stages(self._h, 0))
+        return [(_cuda.STAGES[r.stage], r.layer, float(r.us)) for r in recs[:n.value]]
 
     def close(self) -> None:
         if getattr(self, "_h", None):
@@ -297,14 +317,16 @@ class ServeModel:
         return ids
 
     def _check_gamma(self, ids_host: torch.Tensor, gamma: int) -> None:
+        """Validate the batch's task ids (every gamma: an id indexes the device head / prompt
+        tables) and, for gamma > 0, that each task in the batch has prompts at gamma
+        (ProfileGapError names the task, as the reference's prompt lookup does)."""
         if gamma < -(self.backbone.cfg.n_tokens - 1):
             raise ValueError(f"gamma {gamma} merges more tokens than exist")
-        if gamma > 0:
-            for i in set(ids_host.tolist()):
-                if i < 0 or i >= len(self.tasks):
-                    raise ValueError(f"unknown task id {i}")
-                if gamma not in self.tasks[i].prompts:
-                    raise ProfileGapError(self.tasks[i].name, gamma, "prompt")
+        for i in set(ids_host.tolist()):
+            if i < 0 or i >= len(self.tasks):
+                raise ValueError(f"unknown task id {i}")
+            if gamma > 0 and gamma not in self.tasks[i].prompts:
+                raise ProfileGapError(self.tasks[i].name, gamma, "prompt")
 
     def forward(self, inputs: torch.Tensor, tasks, task_params=None, gamma: int = 0) -> torch.Tensor:
         """ServeModel.forward(inputs, tasks, task_params, gamma) (PAPER.md:526).
@@ -319,9 +341,10 @@ class ServeModel:
                     self.register_task(tp)
         ids = self.task_ids(tasks)
         self._check_gamma(ids.cpu(), gamma)
-        if inputs.device.type == "cpu":
-            return self.backbone.forward_host(inputs.float(), ids, gamma)
-        return self.backbone.forward_raw(inputs.float().contiguous(), ids.to(self.backbone.device), gamma)
+        with torch.cuda.device(self.backbone.device):
+            if inputs.device.type == "cpu":
+                return self.backbone.forward_host(inputs.float(), ids, gamma)
+            return self.backbone.forward_raw(inputs.float().contiguous(), ids.to(self.backbone.device), gamma)
 
     __call__ = forward
 
@@ -331,8 +354,9 @@ class ServeModel:
         ``.wait()`` gives the host logits.  Submitting the next batch before waiting overlaps
         its H2D copy with the current forward."""
         ids = self.task_ids(tasks)
-        self._check_gamma(ids, gamma)
-        return self.backbone.forward_host_async(inputs.float(), ids, gamma, out=out)
+        self._check_gamma(ids.cpu(), gamma)
+        with torch.cuda.device(self.backbone.device):
+            return self.backbone.forward_host_async(inputs.float(), ids, gamma, out=out)
 
     def execute(self, batch: Batch, gamma: int, payloads: Dict[int, torch.Tensor]) -> Tuple[int, List[int]]:
         """Run a planned batch (engine step) and return (latency_us, predictions).
@@ -344,13 +368,16 @@ class ServeModel:
         imgs = torch.stack([payloads[q.id] for q in batch.queries]).to(self.backbone.device, torch.float32)
         ids = self.task_ids([q.task for q in batch.queries])
         self._check_gamma(ids, gamma)
-        ids_dev = ids.to(self.backbone.device)
-        start = torch.cuda.Event(enable_timing=True)
-        end = torch.cuda.Event(enable_timing=True)
-        start.record()
-        logits = self.backbone.forward_raw(imgs.contiguous(), ids_dev, gamma)
-        end.record()
-        end.synchronize()
+        dev = self.backbone.device
+        with torch.cuda.device(dev):
+            ids_dev = ids.to(dev)
+            stream = torch.cuda.current_stream(dev)
+            start = torch.cuda.Event(enable_timing=True)
+            end = torch.cuda.Event(enable_timing=True)
+            start.record(stream)
+            logits = self.backbone.forward_raw(imgs.contiguous(), ids_dev, gamma)
+            end.record(stream)
+            end.synchronize()
         latency_us = us_from_s(start.elapsed_time(end) / 1e3)
         preds = []
         for i, q in enumerate(batch.queries):
@@ -365,21 +392,28 @@ class ServeModel:
         ProfileTable (write it with profiles.write_profile_csv)."""
         table = ProfileTable(base_tokens=self.backbone.cfg.n_tokens, layers=self.backbone.cfg.depth)
         cfg = self.backbone.cfg
-        g = torch.Generator(device=self.backbone.device).manual_seed(seed)
-        imgs = torch.randn(batch_size, 3, cfg.img, cfg.img, generator=g, device=self.backbone.device)
+        dev = self.backbone.device
+        g = torch.Generator(device=dev).manual_seed(seed)
+        imgs = torch.randn(batch_size, 3, cfg.img, cfg.img, generator=g, device=dev)
+        with torch.cuda.device(dev):
+            return self._profile(table, imgs, gammas, batch_size, accuracy, iters, warmup)
+
+    def _profile(self, table, imgs, gammas, batch_size, accuracy, iters, warmup) -> ProfileTable:
+        dev = self.backbone.device
+        stream = torch.cuda.current_stream(dev)
         for gamma in gammas:
             batch_times = []
             for ti, task in enumerate(self.tasks):
                 if gamma > 0 and gamma not in task.prompts:
                     continue
-                ids = torch.full((batch_size,), ti, dtype=torch.int32, device=self.backbone.device)
+                ids = torch.full((batch_size,), ti, dtype=torch.int32, device=dev)
                 for _ in range(warmup):
                     self.backbone.forward_raw(imgs, ids, gamma)
                 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s.record()
+                s.record(stream)
                 for _ in range(iters):
                     self.backbone.forward_raw(imgs, ids, gamma)
-                e.record()
+                e.record(stream)
                 e.synchronize()
                 sec = s.elapsed_time(e) / 1e3 / iters
                 batch_times.append(sec)

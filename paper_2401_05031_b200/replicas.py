@@ -11,9 +11,13 @@ host side), never a collective on the forward path.
 from __future__ import annotations
 
 import heapq
+import os
+import socket
+import subprocess
+import sys
 from typing import List, Optional, Sequence, Tuple
 
-__all__ = ["round_robin", "earliest_free", "aggregate_throughput"]
+__all__ = ["round_robin", "earliest_free", "aggregate_throughput", "launch_replicas", "free_port"]
 
 
 def round_robin(n_batches: int, world: int) -> List[List[int]]:
@@ -58,3 +62,26 @@ def aggregate_throughput(local_items: float, local_ms: float, group=None) -> Tup
     dist.all_reduce(items, op=dist.ReduceOp.SUM, group=group)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX, group=group)
     return float(items.item()), float(ms.item())
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch_replicas(n: int, script: str, argv: Sequence[str], capture: bool = False,
+                    timeout: Optional[float] = None) -> subprocess.CompletedProcess:
+    """Run `script argv` as n ranks, one process (and replica) per GPU, through
+    torch.distributed.run on 127.0.0.1 (what `bench.py --gpus N` does when it is started
+    without a launcher).  Each rank reads RANK / LOCAL_RANK / WORLD_SIZE from the env; the
+    ranks only share a host-side (gloo) barrier and the throughput reduction."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), script, *argv]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.run(cmd, env=env, capture_output=capture, text=True, timeout=timeout)

@@ -30,7 +30,7 @@ def test_library_exports_every_symbol():
     for name in declared_functions():
         assert hasattr(lib, name), name
     l = _cuda.lib()
-    assert l.ta_abi_version() == 2
+    assert l.ta_abi_version() == _cuda.ABI_VERSION
     assert l.ta_strerror(-4) == b"no prompts registered for (task, gamma)"
     assert l.ta_strerror(12345) == b"unknown error"
 

@@ -3,7 +3,7 @@ seeded weights and synthetic images (north_star).
 
 fp32 mode: merge index sets bit-exact (free-running), logits rtol 1e-4 with
 atol 1e-4 * max|logit|.
-bf16 mode: stated tolerance |dlogit| <= BF16_TOL * max|logit| with the oracle's merge
+bf16 mode: stated tolerance |dlogit| <= BF16_TOL * max|logit| (1.5x the measured maximum) with the oracle's merge
 indices forced (teacher forcing), and top-1 unchanged wherever the oracle's top-2 margin
 exceeds twice that bound.  Free-running bf16 index divergence is reported, not asserted."""
 
@@ -14,7 +14,7 @@ from tests import helpers
 
 pytestmark = pytest.mark.gpu
 
-BF16_TOL = 0.03  # relative to max|logit| of the oracle, index-forced
+BF16_TOL = 0.013  # x max|logit| (oracle, index-forced): 1.5 x the largest measured (8.52e-3, profiles/r02_parity.md)
 
 
 def _run(name, gamma, batch, dtype, prompt_mode="accumulate", classes=(10, 100), seed=0,
@@ -44,10 +44,22 @@ def _finite(x):
     return torch.where(torch.isinf(x), torch.zeros_like(x), x)
 
 
+def _bf16_check(name, forced, ref, **meta):
+    """Index-forced bf16 logits vs the fp32 oracle: |dlogit| <= BF16_TOL max|logit|; records the
+    measured relative error (the committed per-config table, profiles/r02_parity.md)."""
+    fr, rf = _finite(forced), _finite(ref)
+    scale = rf.abs().max().item()
+    err = (fr - rf).abs().max().item()
+    helpers.record("bf16_forced", {"case": name, **meta, "max_abs_dlogit": err, "max_logit": scale,
+                                   "rel": err / scale})
+    assert err <= BF16_TOL * scale, (name, err, scale)
+    return fr, rf, err, scale
+
+
 def _assert_indices_equal(tr, gpu_trace):
     assert len(gpu_trace) == len(tr.merges)
     for step, (s, d, u) in zip(tr.merges, gpu_trace):
-        assert torch.equal(s, s) and torch.equal(step.src, s), f"src differs at layer {step.layer}"
+        assert torch.equal(step.src, s), f"src differs at layer {step.layer}"
         assert torch.equal(step.dst, d), f"dst differs at layer {step.layer}"
         assert torch.equal(step.unm, u), f"unm differs at layer {step.layer}"
 
@@ -71,9 +83,7 @@ def test_tiny_bf16(gamma, prompt_mode, fold_ln):
     if gamma <= 0 and prompt_mode == "replace":
         pytest.skip("prompt mode only matters for gamma > 0")
     cfg, ref, tr, out, gtr, forced, _ = _run("vit_tiny", gamma, 6, "bf16", prompt_mode, fold_ln=fold_ln)
-    scale = _finite(ref).abs().max().item()
-    err = (_finite(forced) - _finite(ref)).abs().max().item()
-    assert err <= BF16_TOL * scale, (err, scale)
+    _bf16_check("vit_tiny b=6", forced, ref, gamma=gamma, prompt_mode=prompt_mode, fold_ln=fold_ln)
 
 
 def test_vit_b16_config1_fp32():
@@ -87,11 +97,8 @@ def test_vit_b16_config1_fp32():
 @pytest.mark.parametrize("fold_ln", [True, False])
 def test_vit_b16_config1_bf16(fold_ln):
     cfg, ref, tr, out, gtr, forced, _ = _run("vit_b16", -8, 8, "bf16", fold_ln=fold_ln)
-    fr, rf = _finite(forced), _finite(ref)
-    scale = rf.abs().max().item()
+    fr, rf, err, scale = _bf16_check("vit_b16 b=8 (config 1)", forced, ref, gamma=-8, fold_ln=fold_ln)
     bound = BF16_TOL * scale
-    err = (fr - rf).abs().max().item()
-    assert err <= bound, (err, bound)
     top2 = rf.topk(2, dim=-1).values
     margin = top2[:, 0] - top2[:, 1]
     decisive = margin > 2 * bound
@@ -103,9 +110,7 @@ def test_vit_b16_config1_bf16(fold_ln):
 def test_vit_b16_bf16_sweep_gammas(gamma):
     """The bench's gammas at batch 16 (bf16, LN folded), index-forced."""
     cfg, ref, tr, out, gtr, forced, _ = _run("vit_b16", gamma, 16, "bf16")
-    fr, rf = _finite(forced), _finite(ref)
-    scale = rf.abs().max().item()
-    assert (fr - rf).abs().max().item() <= BF16_TOL * scale
+    _bf16_check("vit_b16 b=16", forced, ref, gamma=gamma)
 
 
 @pytest.mark.parametrize("gamma", [-16, 0, 16])
@@ -113,8 +118,7 @@ def test_vit_l16_config3_bf16(gamma):
     """Config 3 shapes (ViT-L/16; gamma=+16 reaches t=581 -> mma.sync attention fallback),
     batch 2, index-forced bf16 vs the oracle."""
     cfg, ref, tr, out, gtr, forced, _ = _run("vit_l16", gamma, 2, "bf16")
-    fr, rf = _finite(forced), _finite(ref)
-    assert (fr - rf).abs().max().item() <= BF16_TOL * rf.abs().max().item()
+    _bf16_check("vit_l16 b=2", forced, ref, gamma=gamma)
 
 
 def test_vit_l16_fp32_merge_indices():
@@ -134,7 +138,7 @@ def test_vit_h14_config5(dtype):
         _assert_indices_equal(tr, gtr)
         torch.testing.assert_close(_finite(out), _finite(ref), rtol=1e-4, atol=1e-4 * scale)
     else:
-        assert (_finite(forced) - _finite(ref)).abs().max().item() <= BF16_TOL * scale
+        _bf16_check("vit_h14 b=2", forced, ref, gamma=-24)
 
 
 @pytest.mark.parametrize("batch", [1, 3])
@@ -143,10 +147,41 @@ def test_vit_b16_odd_batches(batch, gamma):
     """Batches that fill neither a 128-row tile nor a CTA pair (B*t not a multiple of 256),
     bf16 index-forced and fp32 free-running (merge indices bit-exact)."""
     cfg, ref, tr, out, gtr, forced, _ = _run("vit_b16", gamma, batch, "bf16")
-    rf = _finite(ref)
-    assert (_finite(forced) - rf).abs().max().item() <= BF16_TOL * rf.abs().max().item()
+    _bf16_check(f"vit_b16 b={batch}", forced, ref, gamma=gamma)
     cfg, ref, tr, out, gtr, _, _ = _run("vit_b16", gamma, batch, "fp32")
     if gamma < 0:
         _assert_indices_equal(tr, gtr)
     scale = _finite(ref).abs().max().item()
     torch.testing.assert_close(_finite(out), _finite(ref), rtol=1e-4, atol=1e-4 * scale)
+
+
+@pytest.mark.parametrize("gamma", [-8, 0])
+def test_ln_fold_outlier_channels(gamma):
+    """LayerNorm folding with large-magnitude residual channels (as pretrained ViTs carry): four
+    channels offset by +-40 in every token (patch bias and cls), so the folded GEMM's bf16(x)
+    operand is rounded relative to |x| ~ 40 on them.  Fold and no-fold must both hold the bf16
+    bound against the oracle, and the fold may not be much worse than the explicit LayerNorm."""
+    import copy
+
+    cfg, params = helpers.backbone("vit_b16")
+    params = copy.deepcopy(params)
+    chans, sign = [5, 100, 333, 700], [1.0, -1.0, 1.0, 1.0]
+    for c, sg in zip(chans, sign):
+        params["patch_b"][c] += 40.0 * sg
+        params["cls"][c] += 40.0 * sg
+    tasks = helpers.task_params(cfg, (10, 100), [])
+    imgs = helpers.synthetic_images(8, cfg.img, seed=5)
+    ids = torch.arange(8) % 2
+    ref, tr = helpers.oracle_forward(cfg, params, tasks, imgs, ids, gamma)
+    flat = tr.flat_int32().cuda() if tr.merges else None
+    errs = {}
+    for fold in (True, False):
+        sm = helpers.serve_model(cfg, params, tasks, dtype="bf16", fold_ln=fold)
+        out = sm.backbone.forward_raw(imgs.cuda(), ids.to(torch.int32).cuda(), gamma, forced_trace=flat)
+        torch.cuda.synchronize()
+        _, _, errs[fold], scale = _bf16_check("vit_b16 b=8 outlier channels", out.cpu(), ref, gamma=gamma,
+                                              fold_ln=fold)
+        sm.backbone.close()
+    helpers.record("ln_fold_outliers", {"gamma": gamma, "err_fold": errs[True], "err_nofold": errs[False],
+                                        "max_logit": scale})
+    assert errs[True] <= 2.0 * errs[False] + 0.25 * BF16_TOL * scale, errs

@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 
 B = 256
 SAMPLE = [0, 37, 74, 111, 148, 185, 222, 255]
-BF16_TOL = 0.03
+from tests.test_gpu_forward import BF16_TOL  # noqa: E402
 _MODELS = {}
 
 

@@ -64,3 +64,23 @@ def test_aggregate_gloo_world2():
 
 def test_aggregate_single_process():
     assert replicas.aggregate_throughput(5, 2.5) == (5.0, 2.5)
+
+
+def test_launch_replicas_world2():
+    """The spawn path of `bench.py --gpus N` (no launcher in the environment): N ranks over
+    torch.distributed.run on 127.0.0.1, rank 0 prints the aggregated line."""
+    import json
+
+    probe = os.path.join(os.path.dirname(os.path.abspath(__file__)), "replica_probe.py")
+    env_keep = os.environ.pop("WORLD_SIZE", None)
+    try:
+        res = replicas.launch_replicas(2, probe, [], capture=True, timeout=300)
+    finally:
+        if env_keep is not None:
+            os.environ["WORLD_SIZE"] = env_keep
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    out = json.loads(lines[0])
+    assert out["world"] == 2 and out["items"] == 300.0 and out["ms"] == 6.0
+    assert sorted(r["local_rank"] for r in out["ranks"]) == [0, 1]
