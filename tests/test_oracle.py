@@ -203,3 +203,57 @@ def test_weights_deterministic():
     p = init_prompts(cfg, 4, 0)
     v = math.sqrt(6.0 / (3 * 16 * 16 + cfg.dim))
     assert p.shape == (cfg.depth, 4, cfg.dim) and p.abs().max() <= v
+
+
+# ---------------------------------------------------------------- third-party pin (transformers)
+def _hf_golden_cases():
+    from tests.golden.make_hf_golden import CASES
+
+    return [(n, b, g) for n, b, gs in CASES for g in gs]
+
+
+@pytest.mark.parametrize("name,batch,gamma", _hf_golden_cases())
+def test_oracle_matches_hf_golden(name, batch, gamma):
+    """The oracle (fp64) reproduces the same seeded ViT run through HuggingFace transformers'
+    ViTForImageClassification modules with upstream-structured ToMe / VPT glue
+    (tests/golden/make_hf_golden.py): identical merge traces, logits to fp64 rounding."""
+    gold = np.load(os.path.join(HERE, "golden", "hf_vit_golden.npz"))
+    from paper_2401_05031_b200.config import VIT_CONFIGS
+    from paper_2401_05031_b200.weights import init_head, init_prompts, synthetic_images
+
+    cfg, params = helpers.backbone(name)
+    head = init_head(cfg, 10, 0)
+    tasks = [{"name": "t0", "head": head, "prompts": {gamma: init_prompts(cfg, gamma, 0)} if gamma > 0 else {}}]
+    imgs = synthetic_images(batch, cfg.img, seed=21)
+    key = f"{name}_g{gamma}"
+    logits, tr = helpers.oracle_forward(cfg, params, tasks, imgs, torch.zeros(batch, dtype=torch.int64), gamma,
+                                        dtype=torch.float64)
+    ref = torch.from_numpy(gold[f"{key}_logits"])
+    assert int(gold[f"{key}_nmerge"]) == len(tr.merges)
+    for i, st in enumerate(tr.merges):
+        assert np.array_equal(st.src.numpy(), gold[f"{key}_l{i}_src"]), f"layer {st.layer} src"
+        assert np.array_equal(st.dst.numpy(), gold[f"{key}_l{i}_dst"]), f"layer {st.layer} dst"
+        assert np.array_equal(st.unm.numpy(), gold[f"{key}_l{i}_unm"]), f"layer {st.layer} unm"
+    torch.testing.assert_close(logits, ref, rtol=1e-10, atol=1e-10 * ref.abs().max().item())
+
+
+def test_hf_golden_live():
+    """When transformers is importable (this image, and the GPU box), regenerate one case live
+    from transformers' modules and compare with the oracle: the committed fixture is not stale."""
+    pytest.importorskip("transformers")
+    from tests.golden.make_hf_golden import hf_model, hf_tokenadapt_forward
+    from paper_2401_05031_b200.weights import init_head, synthetic_images
+
+    cfg, params = helpers.backbone("vit_tiny")
+    head = init_head(cfg, 10, 0)
+    p64 = {k: (v.double() if torch.is_tensor(v) else [{kk: vv.double() for kk, vv in l.items()} for l in v])
+           for k, v in params.items()}
+    m = hf_model(cfg, p64, {k: v.double() for k, v in head.items()})
+    imgs = synthetic_images(3, cfg.img, seed=4)
+    hf_logits, hf_trace = hf_tokenadapt_forward(m, cfg, imgs.double(), -5)
+    tasks = [{"name": "t0", "head": head, "prompts": {}}]
+    logits, tr = helpers.oracle_forward(cfg, params, tasks, imgs, torch.zeros(3, dtype=torch.int64), -5,
+                                        dtype=torch.float64)
+    for st, (s, d, u) in zip(tr.merges, hf_trace):
+        assert torch.equal(st.src, s) and torch.equal(st.dst, d) and torch.equal(st.unm, u)
+    torch.testing.assert_close(logits, hf_logits, rtol=1e-10, atol=1e-12)
