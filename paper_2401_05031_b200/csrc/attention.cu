@@ -300,12 +300,14 @@ __global__ void __launch_bounds__(128)
 // pipelined tcgen05 kernel (attention_fa.cu) beyond (1420 vs 1771 us at t = 581, H = 16).
 // head_dim 80 (ViT-H/14): the whole-row tcgen05 kernel with a 16-column SW32 tail for
 // 64 < t <= 512 (1066 vs 1391 us at t = 257, B = 512, H = 16), mma.sync otherwise.
-// TA_ATTENTION_BACKEND=tc / fa / mma forces one kernel (the parity tests cover all three).
+// TA_ATTENTION_BACKEND=tc / fa / mma / tp forces one kernel (the parity tests cover all four).
+// The P-in-TMEM kernel (attention_tp.cu, hd 64, 64 < t <= 256) is correct but measured slower
+// (141 vs 117 us at t = 197, 103 vs 90 us at t = 149; profiles/r02_attn.md), so it is not a default.
 static int attention_backend() {
   static int mode = -1;
   if (mode < 0) {
     const char* v = getenv("TA_ATTENTION_BACKEND");
-    mode = !v ? 0 : v[0] == 'm' ? 1 : v[0] == 't' ? 2 : v[0] == 'f' ? 3 : 0;
+    mode = !v ? 0 : v[0] == 'm' ? 1 : (v[0] == 't' && v[1] == 'c') ? 2 : v[0] == 'f' ? 3 : v[0] == 't' ? 4 : 0;
   }
   return mode;
 }
@@ -317,7 +319,9 @@ int attention(const void* qkv, const float* size, int B, int t, int H, int hd, v
   const int backend = attention_backend();
   if (dtype == TA_DTYPE_BF16 && backend != 1 && !(backend == 0 && t <= 64)) {
     int rc = TA_ERR_SHAPE;
-    if (backend == 2 || (backend == 0 && t <= 512)) rc = attention_tc(qkv, size, B, t, H, hd, out, s);
+    if (backend == 4) rc = attention_tp(qkv, size, B, t, H, hd, out, s);
+    if (rc == TA_ERR_SHAPE && (backend == 2 || ((backend == 0 || backend == 4) && t <= 512)))
+      rc = attention_tc(qkv, size, B, t, H, hd, out, s);
     if (rc == TA_ERR_SHAPE && backend != 2) rc = attention_fa(qkv, size, B, t, H, hd, out, s);
     if (rc != TA_ERR_SHAPE) return rc;  // outside the tcgen05 envelopes -> mma.sync below
   }

@@ -134,6 +134,8 @@ int attention_tc(const void* qkv, const float* size, int B, int t, int H, int hd
                  cudaStream_t s);
 int attention_fa(const void* qkv, const float* size, int B, int t, int H, int hd, void* out,
                  cudaStream_t s);
+int attention_tp(const void* qkv, const float* size, int B, int t, int H, int hd, void* out,
+                 cudaStream_t s);
 int attention(const void* qkv, const float* size, int B, int t, int H, int hd, void* out,
               int dtype, cudaStream_t s);
 

@@ -23,7 +23,11 @@ def main():
     lib = _cuda.lib()
     st = torch.cuda.current_stream().cuda_stream
     shapes = [(7, 1, 64), (5, 33, 64), (6, 64, 64), (4, 65, 64), (3, 197, 64), (2, 261, 64), (2, 300, 64), (2, 389, 64), (2, 449, 64), (2, 513, 64),
-              (2, 581, 64), (5, 65, 80), (4, 185, 80), (3, 233, 80), (3, 257, 80), (2, 300, 80)]
+              (2, 581, 64), (5, 65, 80), (4, 185, 80), (3, 233, 80), (3, 257, 80), (2, 300, 80),
+              # the P-in-TMEM kernel's envelope (64 < t <= 256, hd 64) with several items per CTA:
+              # O at columns 192 (t <= 192) / 128 (gated first PV), one or two query tiles
+              (32, 197, 64), (32, 129, 64), (24, 101, 64), (16, 256, 64), (20, 192, 64), (20, 193, 64),
+              (28, 176, 64), (26, 128, 64), (30, 213, 64), (13, 245, 64)]
     for b, t, hd in shapes:
         for with_size in (False, True):
             heads = 12 if hd == 64 else 16

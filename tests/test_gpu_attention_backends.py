@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-@pytest.mark.parametrize("backend", ["default", "tc", "fa", "mma"])
+@pytest.mark.parametrize("backend", ["default", "tc", "tp", "fa", "mma"])
 def test_attention_backend(backend):
     env = dict(os.environ)
     env.pop("TA_ATTENTION_BACKEND", None)

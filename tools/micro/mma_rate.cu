@@ -42,6 +42,16 @@ __global__ void mma_rate(unsigned long long* out, int iters) {
         }
         continue;
       }
+      if (kMode == 4 || kMode == 5) {  // PV with A = P from TMEM (columns 256.. / 0..), B = V MN-major
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t d = kMode == 4 ? tmem : tmem + 128, at = tmem + 256 + 8 * k;
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d), "r"(at),
+                       "l"(umma_desc_sw128_mn(vbase + k * 2048, 8192, 1024)), "r"(id_pv), "r"(1));
+        }
+        continue;
+      }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         if (kMode == 0) umma_f16(tmem, a + 2 * k, b + 2 * k, id_s, 1);
@@ -63,6 +73,24 @@ __global__ void mma_rate(unsigned long long* out, int iters) {
       for (int j = 0; j < 8; ++j) sts_u4(addr + ((k + j) & 7) * 4096, make_uint4(k, j, k, j));
       ++k;
     }
+  }
+  if (kLoad == 4 && threadIdx.x >= 128) {  // 8 warps: ld 64 columns, st 32 columns (softmax-like)
+    const uint32_t base = slot + ((((threadIdx.x >> 5) & 3) * 32u) << 16) + 256 + 128 * ((threadIdx.x >> 7) & 1);
+    float acc = 0.f;
+    while (!done) {
+      for (int c = 0; c < 128; c += 64) {
+        uint32_t r[32], q[32];
+        tmem_ld_32x32b_x32(base + c, r);
+        tmem_ld_32x32b_x32(base + c + 32, q);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) r[j] = r[2 * j] ^ q[2 * j + 1];
+        tmem_st_32x32b_x16(base + c, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+        tmem_st_wait();
+        acc += __uint_as_float(r[3]);
+      }
+    }
+    if (acc == 1234.f) out[0] = 0;
   }
   if ((kLoad == 1 || kLoad == 3) && threadIdx.x >= 128) {  // 8 warps streaming TMEM loads
     // kLoad 1: columns 256..511 (other half); 3: columns 64..319 (same half as the PV output)
@@ -103,7 +131,13 @@ void run(const char* name, unsigned long long* d, double floor) {
 int main() {
   unsigned long long* d;
   cudaMalloc(&d, 148 * sizeof(unsigned long long));
+  run<0, 0>("S   M128 N256", d, 128);
   run<1, 0>("PV  M128 N64", d, 32);
+  run<4, 0>("PV TS (A in TMEM) N64", d, 32);
+  run<4, 1>("PV TS + ld cols 256..511", d, 32);
+  run<5, 4>("PV TS (D 128..) + ld/st 256..", d, 32);
+  run<1, 4>("PV SS + ld/st 256..", d, 32);
+  run<0, 4>("S N256 + ld/st 256..", d, 128);
   run<1, 1>("PV  + ld cols 256..511", d, 32);
   run<1, 3>("PV  + ld cols 64..319", d, 32);
   run<3, 1>("pattern /4 + ld other half", d, 0);
