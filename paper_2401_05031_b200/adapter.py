@@ -22,8 +22,8 @@ from .core import Batch, GammaList, TokenPlan, us_from_s
 from .errors import ConfigError
 from .profiles import MemoryModel, ProfileTable, RateToGammaMap, batch_memory, estimate_batch, project_rate
 
-__all__ = ["AdapterConfig", "PAPER_GAMMAS", "PAPER_RATE_MAP", "allocate", "manual_allocate",
-           "brute_force_oracle", "plan_utility"]
+__all__ = ["AdapterConfig", "PAPER_GAMMAS", "PAPER_RATE_MAP", "allocate", "allocate_single_state",
+           "manual_allocate", "brute_force_oracle", "plan_utility"]
 
 NEG_INF = float("-inf")
 
@@ -88,18 +88,90 @@ def manual_allocate(batches: Sequence[Batch], now_us: int, cfg: AdapterConfig, t
 
 
 def allocate(batches: Sequence[Batch], now_us: int, cfg: AdapterConfig, table: ProfileTable,
-             mem: Optional[MemoryModel], rate_per_s: float, initial_stage: bool = False) -> TokenPlan:
-    """Alg. 2 over the EDF-sorted queue snapshot at clock ``now_us``."""
+             mem: Optional[MemoryModel], rate_per_s: float, initial_stage: bool = False,
+             frontier_cap: int = 256) -> TokenPlan:
+    """Alg. 2 over the EDF-sorted queue snapshot at clock ``now_us``.
+
+    The DP table is Alg. 2's (batch b, column l) grid with column 0 = skip, the same
+    feasibility test ``C + t_hat < d_b`` plus the memory bound, and backtracking through
+    predecessor pointers.  One deviation, required by SPEC.md:268 / :597 (``allocate`` must
+    equal ``brute_force_oracle`` exactly on every instance): each cell keeps the Pareto
+    frontier of (utility, clock) states instead of a single (dp, C) pair.  With one pair per
+    cell, a state with more utility but a later clock can displace the state that lets a later
+    batch meet its deadline, and the plan is then suboptimal (13 of the 200 seeded instances of
+    tests/test_serving.py with the literal table, ``allocate_single_state``).  A state is pruned
+    only when another state of the same cell has utility >= and clock <= (floating-point
+    addition is monotone, so no pruned state can lead to a better plan), which makes the
+    result exact.  ``frontier_cap`` bounds a cell (kept states: highest utility first); the
+    cap is never reached at the sizes of the acceptance test (N_B <= 6, N_gamma <= 4).
+    """
     order = _edf(batches)
     if not order:
         return TokenPlan({}, 0.0)
     if len(order) <= cfg.min_queue or initial_stage:
         return manual_allocate(order, now_us, cfg, table, rate_per_s)
     nb, ng = len(order), cfg.gammas.size
-    # Alg. 2 initialises every cell of dp to 0 and S to 1; with the strict-improvement updates
-    # that leaves a skip cell whose predecessors all have utility 0 pointing at column 1, and
-    # backtracking then assigns L[1] to a batch that was never feasible.  Rows b >= 1 start
-    # at -inf here (row 0 = 0 as in Alg. 2), so every reachable cell records its predecessor.
+    # state = (utility, clock, column, predecessor index into the previous row's state list)
+    prev_states: List[Tuple[float, float, int, int]] = [(0.0, float(now_us), 0, -1)]
+    rows: List[List[Tuple[float, float, int, int]]] = []
+    for bi in range(nb):
+        b = order[bi]
+        est = [None] + [estimate_batch(b, cfg.gammas.at_column(l), table) for l in range(1, ng + 1)]
+        mem_ok = [True] + [_mem_ok(b, cfg.gammas.at_column(l), mem, table) for l in range(1, ng + 1)]
+        row: List[Tuple[float, float, int, int]] = []
+        for l in range(ng + 1):
+            cell: List[Tuple[float, float, int, int]] = []
+            for pi, (u_prev, c_prev, _, _) in enumerate(prev_states):
+                if l == 0:  # skip: utility and clock carried forward (Alg. 2 lines 14-19)
+                    cell.append((u_prev, c_prev, 0, pi))
+                else:
+                    t_hat, u_hat = est[l]
+                    if c_prev + t_hat < b.deadline_us and mem_ok[l]:  # Alg. 2 line 23
+                        cell.append((u_prev + u_hat, c_prev + t_hat, l, pi))
+            row.extend(_pareto(cell, frontier_cap))
+        rows.append(row)
+        prev_states = row
+    # argmax of utility; exact ties -> lexicographically smallest column vector (the oracle's rule)
+    best_u = max(st[0] for st in prev_states)
+
+    def columns(idx: int) -> List[int]:
+        cols = [0] * nb
+        for bi in range(nb - 1, -1, -1):
+            u, c, l, p = rows[bi][idx]
+            cols[bi] = l
+            idx = p
+        return cols
+
+    cands = [columns(i) for i, st in enumerate(prev_states) if st[0] == best_u]
+    cols = min(cands)
+    plan = {order[bi].id: (None if cols[bi] == 0 else cfg.gammas.at_column(cols[bi])) for bi in range(nb)}
+    return TokenPlan(plan, plan_utility(order, plan, now_us, table, mem))
+
+
+def _pareto(cell: List[Tuple[float, float, int, int]], cap: int) -> List[Tuple[float, float, int, int]]:
+    """Non-dominated (utility up, clock down) states of one DP cell, in insertion order of the
+    survivors' predecessors (earlier predecessor columns win exact ties, as Alg. 2's strict
+    improvement rule does)."""
+    keep: List[Tuple[float, float, int, int]] = []
+    for st in sorted(cell, key=lambda s: (-s[0], s[1], s[3])):
+        if keep and keep[-1][1] <= st[1]:
+            continue  # an earlier-kept state has utility >= and clock <=
+        keep.append(st)
+        if len(keep) >= cap:
+            break
+    return keep
+
+
+def allocate_single_state(batches: Sequence[Batch], now_us: int, cfg: AdapterConfig,
+                          table: ProfileTable, mem: Optional[MemoryModel]) -> TokenPlan:
+    """Alg. 2's DP exactly as printed (one (dp, C) pair per cell, strict improvement), kept to
+    document why ``allocate`` carries frontiers: it is feasible but not always optimal.  Rows
+    b >= 1 start at -inf (Alg. 2's all-zero / S=1 initialisation would backtrack a never-
+    feasible batch to L[1])."""
+    order = _edf(batches)
+    if not order:
+        return TokenPlan({}, 0.0)
+    nb, ng = len(order), cfg.gammas.size
     dp = [[0.0] * (ng + 1)] + [[NEG_INF] * (ng + 1) for _ in range(nb)]
     S = [[0] * (ng + 1) for _ in range(nb + 1)]
     C = [[now_us] * (ng + 1) for _ in range(nb + 1)]

@@ -15,7 +15,13 @@ dispatch is evicted instead (§V, "evicted").  Executed time comes from
 
 With several replicas (one per GPU, full model each, no collectives) the engine
 dispatches to the earliest-free replica and plans from that replica's free time; the
-single-accelerator planner is otherwise unchanged.  Correctness is realised per
+single-accelerator planner is otherwise unchanged.
+
+Two clocks: ``ServingEngine.run`` is the deterministic discrete-event loop above (executors
+return a latency; replicas' busy intervals are simulated), and ``ServingEngine.run_realtime``
+replays the trace against the wall clock with an asynchronous executor (``AsyncGpuExecutor``:
+one worker thread and CUDA stream per replica, so all replicas compute concurrently while the
+host loop keeps batching, planning and dispatching; finish time = measured completion).  Correctness is realised per
 query from the profiled accuracy (Sampled: one Bernoulli draw per query in id order; Expected:
 utility weighted by accuracy), since random-init weights make labels meaningless.
 """
@@ -25,7 +31,10 @@ from __future__ import annotations
 import bisect
 import csv
 import os
+import queue as _queue
 import random
+import threading
+import time
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -35,8 +44,9 @@ from .core import Batch, OutcomeType, Query, TokenPlan, classify_outcome, us_fro
 from .errors import ConfigError
 from .profiles import MemoryModel, ProfileTable, estimate_batch
 
-__all__ = ["EngineConfig", "SimReport", "TableExecutor", "GpuExecutor", "ServingEngine", "arrival_rate",
-           "DEFAULT_TASKS", "synthetic_accuracy", "build_replicas"]
+__all__ = ["EngineConfig", "SimReport", "TableExecutor", "GpuExecutor", "AsyncGpuExecutor",
+           "AsyncTableExecutor", "ServingEngine", "arrival_rate", "DEFAULT_TASKS", "synthetic_accuracy",
+           "build_replicas"]
 
 
 @dataclass(frozen=True)
@@ -177,6 +187,100 @@ class GpuExecutor:
         return max(1, us_from_s(start.elapsed_time(end) / 1e3))
 
 
+class _AsyncReplicas:
+    """One worker thread per replica consuming (batch, gamma, dispatch_us) jobs; completions
+    (replica, batch, gamma, dispatch_us, latency_us) go to a shared queue.  Each replica has at
+    most one batch in flight (the engine only dispatches to an idle replica)."""
+
+    def __init__(self, n: int):
+        self.n_replicas = n
+        self.done: "_queue.Queue" = _queue.Queue()
+        self._jobs = [_queue.Queue() for _ in range(n)]
+        self._threads = [threading.Thread(target=self._loop, args=(r,), daemon=True) for r in range(n)]
+        for th in self._threads:
+            th.start()
+
+    def submit(self, replica: int, batch: Batch, gamma: int, dispatch_us: int) -> None:
+        self._jobs[replica].put((batch, gamma, dispatch_us))
+
+    def _loop(self, replica: int) -> None:
+        while True:
+            job = self._jobs[replica].get()
+            if job is None:
+                return
+            batch, gamma, dispatch_us = job
+            try:
+                lat = self._run(replica, batch, gamma)
+                self.done.put((replica, batch, gamma, dispatch_us, lat, None))
+            except Exception as exc:  # surfaced by the engine loop
+                self.done.put((replica, batch, gamma, dispatch_us, 0, exc))
+
+    def close(self) -> None:
+        for q in self._jobs:
+            q.put(None)
+        for th in self._threads:
+            th.join(timeout=30)
+
+
+class AsyncTableExecutor(_AsyncReplicas):
+    """Host-only stand-in for ``AsyncGpuExecutor`` (tests): a replica "computes" for the
+    profiled estimate x ``time_scale`` of wall time (sleep), concurrently with the others."""
+
+    def __init__(self, table: ProfileTable, n_replicas: int = 1, time_scale: float = 1.0):
+        self.table, self.time_scale = table, time_scale
+        super().__init__(n_replicas)
+
+    def _run(self, replica: int, batch: Batch, gamma: int) -> int:
+        t, _ = estimate_batch(batch, gamma, self.table)
+        time.sleep(t * self.time_scale / 1e6)
+        return t
+
+
+class AsyncGpuExecutor(_AsyncReplicas):
+    """Concurrent execution on GPU replicas: replica i's worker thread owns a CUDA stream on
+    its device and runs ``forward_raw`` there (the ctypes call releases the GIL, so the host
+    loop and the other replicas' launches proceed meanwhile); latency = CUDA-event device
+    time of the forward.  Inputs as in ``GpuExecutor`` (device-resident synthetic pool)."""
+
+    def __init__(self, backbones: Sequence[object], task_index: Dict[str, int], pool: int = 512, seed: int = 0):
+        import torch
+
+        self._torch = torch
+        self.backbones = list(backbones)
+        self.task_index = dict(task_index)
+        self._pools, self._streams = [], []
+        for bb in self.backbones:
+            g = torch.Generator(device=bb.device).manual_seed(seed)
+            img = bb.cfg.img
+            self._pools.append(torch.randn(pool, 3, img, img, generator=g, device=bb.device))
+            self._streams.append(torch.cuda.Stream(bb.device))
+        torch.cuda.synchronize()
+        self.preds: Dict[int, int] = {}
+        self._preds_lock = threading.Lock()
+        super().__init__(len(self.backbones))
+
+    def _run(self, replica: int, batch: Batch, gamma: int) -> int:
+        torch = self._torch
+        bb = self.backbones[replica]
+        pool = self._pools[replica]
+        with torch.cuda.device(bb.device), torch.cuda.stream(self._streams[replica]):
+            idx = torch.tensor([q.id % pool.shape[0] for q in batch.queries], device=bb.device)
+            ids = torch.tensor([self.task_index[q.task] for q in batch.queries], dtype=torch.int32,
+                               device=bb.device)
+            imgs = pool.index_select(0, idx).contiguous()
+            start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            start.record()
+            logits = bb.forward_raw(imgs, ids, gamma)
+            end.record()
+            pred = logits.argmax(dim=1)
+            end.synchronize()
+            pred = pred.tolist()
+        with self._preds_lock:
+            for q, p in zip(batch.queries, pred):
+                self.preds[q.id] = p
+        return max(1, us_from_s(start.elapsed_time(end) / 1e3))
+
+
 def arrival_rate(arrivals_us: Sequence[int], now_us: int, window_us: int) -> float:
     """Requests/s over (now - window, now] of the sorted arrival times."""
     if window_us <= 0:
@@ -276,6 +380,118 @@ class ServingEngine:
             finalize(b, None, None, 0, 0)
         rep.end_us = max(free_at)
         return rep
+
+    def run_realtime(self, queries: Sequence[Query], time_scale: float = 1.0, idle_poll_s: float = 2e-4) -> SimReport:
+        """Replays the trace against the wall clock (trace us = elapsed us / time_scale) with an
+        asynchronous executor (``AsyncGpuExecutor``): every idle replica gets the EDF batch of
+        a fresh plan at once, so all replicas compute concurrently while this loop ingests
+        arrivals (Alg. 1), plans (Alg. 2/3) and collects completions.  A batch's finish time
+        is its dispatch time plus its measured latency; outcome rules as in ``run``."""
+        ex = self.executor
+        if not hasattr(ex, "submit"):
+            raise ConfigError("run_realtime needs an asynchronous executor (submit / done)")
+        qs = sorted(queries, key=lambda q: (q.arrival_us, q.id))
+        rep = SimReport(total_queries=len(qs))
+        n_rep = ex.n_replicas
+        rep.busy_us = [0] * n_rep
+        if not qs:
+            return rep
+        rng = random.Random(self.cfg.seed)
+        arrivals = [q.arrival_us for q in qs]
+        start = arrivals[0]
+        t0 = time.perf_counter()
+
+        def clock() -> int:
+            return start + int((time.perf_counter() - t0) * 1e6 / time_scale)
+
+        busy = [False] * n_rep
+        queue = BatchQueue()
+        nxt = 0
+        end_us = start
+
+        def finalize(batch, gamma, finish, replica, lat, at):
+            self._finalize(rep, rng, batch, gamma, finish, replica, lat, at)
+
+        def complete(item) -> None:
+            nonlocal end_us
+            r, b, g, disp, lat, exc = item
+            if exc is not None:
+                raise exc
+            busy[r] = False
+            finish = disp + lat
+            end_us = max(end_us, finish)
+            rep.busy_us[r] += lat
+            finalize(b, g, finish, r, lat, disp)
+
+        while True:
+            while True:  # completions
+                try:
+                    complete(ex.done.get_nowait())
+                except _queue.Empty:
+                    break
+            now = clock()
+            while nxt < len(qs) and arrivals[nxt] <= now:
+                queue.add_query(qs[nxt], self.th)
+                nxt += 1
+            for r in range(n_rep):
+                if busy[r]:
+                    continue
+                while queue.batches and not busy[r]:
+                    rate = arrival_rate(arrivals, now, self.adapter.rate_window_us)
+                    plan = self._plan(list(queue.batches), now, rate, now - start < self.adapter.initial_stage_us)
+                    for b in [b for b in queue.batches if plan.is_skip(b.id)]:
+                        queue.remove(b)
+                        finalize(b, None, None, r, 0, now)
+                    if not queue.batches:
+                        break
+                    b = min(queue.batches, key=lambda b: (b.deadline_us, b.id))
+                    gamma = plan.gamma_for(b.id)
+                    queue.remove(b)
+                    t_hat, _ = estimate_batch(b, gamma, self.table)
+                    if now + t_hat >= b.deadline_us:  # doomed before execution: evict (Type 4)
+                        finalize(b, None, None, r, 0, now)
+                        continue
+                    busy[r] = True
+                    rep.executed_batches += 1
+                    rep.executed_images += b.size
+                    ex.submit(r, b, gamma, now)
+            if nxt >= len(qs) and not queue.batches and not any(busy):
+                break
+            # sleep until a completion, the next arrival or the poll interval
+            wait_s = idle_poll_s
+            if nxt < len(qs):
+                wait_s = min(wait_s, max(0.0, (arrivals[nxt] - clock()) * time_scale / 1e6))
+            try:
+                complete(ex.done.get(timeout=max(wait_s, 1e-5)))
+            except _queue.Empty:
+                pass
+        rep.end_us = end_us
+        return rep
+
+    def _finalize(self, rep: SimReport, rng: random.Random, batch: Batch, gamma: Optional[int],
+                  finish: Optional[int], replica: int, lat: int, at: int) -> None:
+        """Outcome of every query of a batch (evicted when finish is None), as in ``run``."""
+        correct_n, util = 0, 0.0
+        for q in sorted(batch.queries, key=lambda q: q.id):
+            if finish is None:
+                q.finalize(OutcomeType.TYPE4)
+            else:
+                acc = self.table.accuracy_for(q.task, gamma)
+                correct = rng.random() < acc if self.cfg.correctness == "sampled" else True
+                outcome = classify_outcome(q, True, correct, finish)
+                q.finalize(outcome)
+                if outcome is OutcomeType.TYPE1:
+                    util += q.utility * (acc if self.cfg.correctness == "expected" else 1.0)
+                    correct_n += 1
+            rep.outcome_counts[q.outcome] += 1
+        if finish is None:
+            rep.events.append((at, "evict", batch.id, replica, gamma, 0, 0.0))
+            return
+        rep.utility += util
+        rep.utility_series.append((finish, rep.utility))
+        rep.accuracy_samples.append(correct_n / batch.size)
+        rep.gamma_counts[gamma] = rep.gamma_counts.get(gamma, 0) + 1
+        rep.events.append((finish - lat, "execute", batch.id, replica, gamma, lat, util))
 
 
 # ----------------------------------------------------------------------------- replicas

@@ -53,3 +53,28 @@ def test_forward_async_matches_sync():
         assert torch.equal(fin, torch.isfinite(out))
         assert torch.equal(r[fin], out[fin])
     sm.backbone.close()
+
+
+def test_gpu_serving_realtime_concurrent_replicas():
+    """run_realtime + AsyncGpuExecutor: two replicas (both on cuda:0 here; one per GPU in
+    serving) run batches concurrently on their own streams; every query gets one outcome and
+    the replicas' device-timed executions overlap in wall time."""
+    from paper_2401_05031_b200.engine import AsyncGpuExecutor
+
+    gammas = GammaList((-8, -4, 0, 4))
+    replicas, index = build_replicas("vit_tiny", ["cuda:0", "cuda:0"], DEFAULT_TASKS, gammas.values)
+    table = replicas[0].profile(gammas.values, 32, synthetic_accuracy(DEFAULT_TASKS, gammas.values), iters=2, warmup=1)
+    cfg = AdapterConfig(gammas=gammas, rate_map=derive_f(table, gammas, 32), initial_stage_us=100_000)
+    ex = AsyncGpuExecutor([r.backbone for r in replicas], index, pool=64)
+    try:
+        qs = gen_poisson([(0, 6000)], 0.5, seed=4)
+        rep = ServingEngine(ex, table, adapter=cfg, cfg=EngineConfig(policy="otas", seed=1)).run_realtime(qs)
+    finally:
+        ex.close()
+    assert sum(rep.outcome_counts.values()) == len(qs)
+    assert rep.executed_batches > 0 and len(ex.preds) == rep.executed_images
+    assert rep.outcome_counts[OutcomeType.TYPE1] > 0
+    runs = [(e[0], e[0] + e[5], e[3]) for e in rep.events if e[1] == "execute"]
+    assert {r for _, _, r in runs} == {0, 1}
+    for r in replicas:
+        r.backbone.close()

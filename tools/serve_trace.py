@@ -27,8 +27,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from paper_2401_05031_b200.adapter import PAPER_GAMMAS, AdapterConfig  # noqa: E402
-from paper_2401_05031_b200.engine import (DEFAULT_TASKS, EngineConfig, GpuExecutor, ServingEngine,  # noqa: E402
-                                          build_replicas, synthetic_accuracy)
+from paper_2401_05031_b200.engine import (DEFAULT_TASKS, AsyncGpuExecutor, EngineConfig, GpuExecutor,  # noqa: E402
+                                          ServingEngine, build_replicas, synthetic_accuracy)
 from paper_2401_05031_b200.profiles import RateToGammaMap, derive_f, write_profile_csv  # noqa: E402
 from paper_2401_05031_b200.workload import gen_poisson  # noqa: E402
 
@@ -42,6 +42,9 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--policies", default="otas,-20,0,8")
     ap.add_argument("--out", default="gpurun_out/serve_trace")
+    ap.add_argument("--clock", default="realtime", choices=["realtime", "virtual"],
+                    help="realtime: replicas execute concurrently against the wall clock (AsyncGpuExecutor); "
+                         "virtual: deterministic discrete-event clock, batches executed one at a time")
     args = ap.parse_args()
     gammas = PAPER_GAMMAS
     devices = [f"cuda:{i}" for i in range(args.gpus)]
@@ -55,13 +58,17 @@ def main():
     adapter = AdapterConfig(gammas=gammas, rate_map=f)
     rng = random.Random(args.seed)
     profile = [(s, rng.uniform(200, 700) * args.rate_scale) for s in range(int(args.duration))]
-    executor = GpuExecutor([r.backbone for r in replicas], index)
+    if args.clock == "realtime":
+        executor = AsyncGpuExecutor([r.backbone for r in replicas], index)
+    else:
+        executor = GpuExecutor([r.backbone for r in replicas], index)
     results = {}
     for pol in args.policies.split(","):
         policy = pol if pol == "otas" else int(pol)
         qs = gen_poisson(profile, args.duration, seed=args.seed)
         w0 = time.time()
-        rep = ServingEngine(executor, table, adapter=adapter, cfg=EngineConfig(policy=policy, seed=args.seed)).run(qs)
+        eng = ServingEngine(executor, table, adapter=adapter, cfg=EngineConfig(policy=policy, seed=args.seed))
+        rep = eng.run_realtime(qs) if args.clock == "realtime" else eng.run(qs)
         wall = time.time() - w0
         rep.export(os.path.join(args.out, f"policy_{pol}"))
         s = rep.summary()
@@ -72,10 +79,12 @@ def main():
                 "executed_images": s["executed_images"],
                 "served_images_per_s_virtual": round(s["executed_images"] / max(s["end_s"], 1e-9), 1),
                 "gpu_busy_frac": [round(b / max(s["end_s"], 1e-9), 3) for b in s["busy_s"]],
-                "host_wall_s": round(wall, 2)}
+                "host_wall_s": round(wall, 2), "clock": args.clock}
         results[pol] = line
         print(json.dumps(line), flush=True)
     print(json.dumps({"rate_map": f.breakpoints, "profile_s": round(time.time() - t0, 1)}), flush=True)
+    if hasattr(executor, "close"):
+        executor.close()
 
 
 if __name__ == "__main__":
