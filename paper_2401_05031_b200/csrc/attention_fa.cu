@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bars.o_full(g), 1);
       mbar_init(bars.o_free(g), 256);
       for (int s = 0; s < 2; ++s) {
-        mbar_init(bars.w_full(g, s), 1);
+        mbar_init(bars.w_full(g, s), 32);
         mbar_init(bars.w_free(g, s), 256);
       }
     }
@@ -262,8 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t s_w = smem_u32(smem + L.w_off) + (2 * g + wb) * L.t_pad * 4;
         for (int j = static_cast<int>(lane); j < L.t_pad; j += 32)
           sts_f32(s_w + j * 4, j < t ? __ldg(size + row_base + j) : 0.f);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bars.w_full(g, wb));
+        mbar_arrive(bars.w_full(g, wb));  // every writer lane releases its own stores
       }
       if (lane == 0) {
         mbar_wait(bars.q_free(g), (n & 1) ^ 1);

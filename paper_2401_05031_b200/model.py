@@ -308,6 +308,13 @@ class ServeModel:
         self.task_index[task.name] = idx
         return idx
 
+    def register_from(self, repo, tasks: Optional[Sequence[str]] = None,
+                      gammas: Optional[Sequence[int]] = None) -> List[int]:
+        """Register tasks of a ``PromptRepository`` (all by default) with this replica: heads and
+        the prompts for ``gammas`` (default: every stored gamma).  Returns their task ids."""
+        return [self.register_task(repo.task_model(t, list(gammas) if gammas is not None else None))
+                for t in (tasks if tasks is not None else repo.tasks())]
+
     def task_ids(self, tasks: Union[Sequence[str], Sequence[int], torch.Tensor]) -> torch.Tensor:
         if isinstance(tasks, torch.Tensor):
             ids = tasks.to(torch.int32)

@@ -19,7 +19,8 @@ import torch
 from .config import ViTConfig
 
 __all__ = ["init_backbone", "init_head", "init_prompts", "synthetic_images", "from_timm_state_dict",
-           "to_timm_state_dict", "load_checkpoint"]
+           "to_timm_state_dict", "load_checkpoint", "head_from_timm_state_dict", "from_hf_vit_state_dict",
+           "head_from_hf_vit_state_dict"]
 
 
 def _trunc_normal(shape, std: float, g: torch.Generator) -> torch.Tensor:
@@ -155,3 +156,62 @@ def load_checkpoint(path: str, cfg: ViTConfig) -> Dict[str, object]:
             if isinstance(sd, dict) and key in sd and isinstance(sd[key], dict):
                 sd = sd[key]
     return from_timm_state_dict(sd, cfg)
+
+
+def head_from_timm_state_dict(sd: Dict[str, torch.Tensor], cfg: ViTConfig) -> Dict[str, torch.Tensor]:
+    """timm ``head.weight`` [C, D] / ``head.bias`` [C] -> a task head {"w", "b"} (fp32), the
+    classifier of one TaskModel."""
+    w = sd["head.weight"].detach().to("cpu", torch.float32).contiguous()
+    b = sd["head.bias"].detach().to("cpu", torch.float32).contiguous()
+    if w.dim() != 2 or w.shape[1] != cfg.dim or tuple(b.shape) != (w.shape[0],):
+        raise ValueError(f"head: expected [C, {cfg.dim}] / [C], got {tuple(w.shape)} / {tuple(b.shape)}")
+    return {"w": w, "b": b}
+
+
+# HuggingFace transformers ViT (models/vit/modeling_vit.py; the same architecture as timm's, with
+# q / k / v as three Linear layers): a second checkpoint format that is installed offline here.
+_HF_LAYER = {"ln1_w": "layernorm_before.weight", "ln1_b": "layernorm_before.bias",
+             "proj_w": "attention.output.dense.weight", "proj_b": "attention.output.dense.bias",
+             "ln2_w": "layernorm_after.weight", "ln2_b": "layernorm_after.bias",
+             "fc1_w": "intermediate.dense.weight", "fc1_b": "intermediate.dense.bias",
+             "fc2_w": "output.dense.weight", "fc2_b": "output.dense.bias"}
+
+
+def from_hf_vit_state_dict(sd: Dict[str, torch.Tensor], cfg: ViTConfig) -> Dict[str, object]:
+    """``ViTModel`` / ``ViTForImageClassification`` state dict (keys with or without the
+    ``vit.`` prefix) -> fp32 master weights; q / k / v are concatenated in that order (the
+    qkv row order s*D + h*hd + j of include/tokadapt_cuda.h)."""
+    pre = "vit." if any(k.startswith("vit.") for k in sd) else ""
+
+    def get(name, shape):
+        t = sd[pre + name].detach().to("cpu", torch.float32)
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+        return t.contiguous()
+
+    d, p, n, m = cfg.dim, cfg.patch, cfg.n_tokens, cfg.mlp_dim
+    params: Dict[str, object] = {
+        "patch_w": get("embeddings.patch_embeddings.projection.weight", (d, 3, p, p)),
+        "patch_b": get("embeddings.patch_embeddings.projection.bias", (d,)),
+        "cls": get("embeddings.cls_token", (1, 1, d)).reshape(d),
+        "pos": get("embeddings.position_embeddings", (1, n, d)).reshape(n, d),
+        "norm_w": get("layernorm.weight", (d,)),
+        "norm_b": get("layernorm.bias", (d,)),
+    }
+    shapes = {"ln1_w": (d,), "ln1_b": (d,), "proj_w": (d, d), "proj_b": (d,), "ln2_w": (d,), "ln2_b": (d,),
+              "fc1_w": (m, d), "fc1_b": (m,), "fc2_w": (d, m), "fc2_b": (d,)}
+    layers = []
+    for i in range(cfg.depth):
+        base = f"encoder.layer.{i}."
+        lw = {k: get(base + v, shapes[k]) for k, v in _HF_LAYER.items()}
+        att = base + "attention.attention."
+        lw["qkv_w"] = torch.cat([get(att + f"{s}.weight", (d, d)) for s in ("query", "key", "value")], 0)
+        lw["qkv_b"] = torch.cat([get(att + f"{s}.bias", (d,)) for s in ("query", "key", "value")], 0)
+        layers.append(lw)
+    params["layers"] = layers
+    return params
+
+
+def head_from_hf_vit_state_dict(sd: Dict[str, torch.Tensor], cfg: ViTConfig) -> Dict[str, torch.Tensor]:
+    """``ViTForImageClassification`` ``classifier.weight`` / ``classifier.bias`` -> task head."""
+    return head_from_timm_state_dict({"head.weight": sd["classifier.weight"], "head.bias": sd["classifier.bias"]}, cfg)

@@ -110,3 +110,33 @@ def test_two_devices_one_process():
         assert torch.cuda.current_device() == 0
         bb.close()
     assert torch.equal(outs[0], outs[1])
+
+
+def test_hf_checkpoint_end_to_end(tmp_path):
+    """transformers ViTForImageClassification checkpoint -> from_hf_vit_state_dict -> GPU replica,
+    head registered through a PromptRepository: logits match transformers' own forward of the
+    same checkpoint (bf16 bound; fp32 mode rtol 1e-4)."""
+    pytest.importorskip("transformers")
+    from paper_2401_05031_b200.model import ServeModel, TransformerModel
+    from paper_2401_05031_b200.repository import PromptRepository
+    from paper_2401_05031_b200.weights import from_hf_vit_state_dict, head_from_hf_vit_state_dict
+    from tests.golden.make_hf_golden import hf_model
+    from tests.test_gpu_forward import BF16_TOL
+
+    cfg, params = helpers.backbone("vit_tiny", seed=7)
+    head = helpers.init_head(cfg, 10, 7)
+    sd = hf_model(cfg, params, head).float().state_dict()
+    repo = PromptRepository(str(tmp_path))
+    h = head_from_hf_vit_state_dict(sd, cfg)
+    repo.register_task("hf_task", h["w"], h["b"])
+    imgs = helpers.synthetic_images(4, cfg.img, seed=9)
+    with torch.no_grad():
+        ref = hf_model(cfg, params, head).float()(pixel_values=imgs).logits
+    for dtype, tol in (("fp32", 1e-4), ("bf16", BF16_TOL)):
+        bb = TransformerModel(cfg, from_hf_vit_state_dict(sd, cfg), "cuda:0", dtype=dtype, n_tasks=1, max_classes=10)
+        sm = ServeModel(bb)
+        sm.register_from(repo)
+        out = sm.forward(imgs.cuda(), ["hf_task"] * 4, gamma=0).cpu()
+        scale = ref.abs().max().item()
+        assert (out - ref).abs().max().item() <= tol * scale, dtype
+        bb.close()
