@@ -24,14 +24,19 @@ enum EpiKind : int {
   // with mu / rstd from ln_stats[m] (eps 1e-6, biased variance):
   EPI_LN_BIAS = 6,     // out(bf16) = LN(x) W^T + b        (QKV)
   EPI_LN_GELU = 7,     // out(bf16) = gelu(LN(x) W^T + b)  (fc1)
+  // proj + residual with the ToMe merge's row movement fused in (bf16 path, LN folded): input
+  // row m goes to row_map[m] of x' (fp32) with its bf16 copy and row statistics, or -- a merged
+  // source token, row_map[m] = -1 - k -- to row k of `side`; merge_fixup then finishes the
+  // destination rows (size-weighted averages) and the size vector.
+  EPI_BIAS_RESID_MERGE = 8,
 };
 
 __host__ __device__ constexpr bool epi_is_stats(int e) {
-  return e == EPI_BIAS_RESID_STATS || e == EPI_PATCH_STATS;
+  return e == EPI_BIAS_RESID_STATS || e == EPI_PATCH_STATS || e == EPI_BIAS_RESID_MERGE;
 }
 __host__ __device__ constexpr bool epi_is_ln(int e) { return e == EPI_LN_BIAS || e == EPI_LN_GELU; }
 __host__ __device__ constexpr bool epi_is_resid(int e) {
-  return e == EPI_BIAS_RESID || e == EPI_BIAS_RESID_STATS;
+  return e == EPI_BIAS_RESID || e == EPI_BIAS_RESID_STATS || e == EPI_BIAS_RESID_MERGE;
 }
 __host__ __device__ constexpr bool epi_is_patch(int e) { return e == EPI_PATCH || e == EPI_PATCH_STATS; }
 __host__ __device__ constexpr bool epi_is_gelu(int e) { return e == EPI_BIAS_GELU || e == EPI_LN_GELU; }
@@ -58,6 +63,10 @@ struct GemmEpi {
   const float* c1 = nullptr;        // consumer: [N]
   const float* c2 = nullptr;        // consumer: [N]
   float inv_dim = 0.f;              // consumer: 1 / D
+  // EPI_BIAS_RESID_MERGE: output row of input row m (>= 0: row of out / xh / stats; < 0: row
+  // -1 - value of side), from merge_map
+  const int32_t* row_map = nullptr;
+  float* side = nullptr;
   int skip = 0;                     // profiling only (TA_GEMM_SKIP_EPILOGUE=1): no epilogue work
   int direct_store = 0;             // TA_GEMM_STORE=direct: STG.256 rows instead of TMA boxes
 };
@@ -90,6 +99,7 @@ inline void attr_done(unsigned long long& mask) {
 
 // Programmatic dependent launch on every kernel (TA_PDL=0 disables it: profiling A/B).
 int pdl_enabled();
+int merge_fusion_enabled();
 
 struct HeadDesc {
   const float* w;  // [classes, D]
@@ -102,6 +112,8 @@ int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, b
               const GemmEpi& epi, cudaStream_t stream);
 int gemm_f32(const float* A, const float* W, int M, int N, int K, int epi_kind,
              const GemmEpi& epi, cudaStream_t stream);
+// Whether gemm_bf16 runs (M, N) on the CTA-pair kernel (the only one with EPI_BIAS_RESID_MERGE).
+bool gemm_pair_path(int M, int N);
 
 // rowops.cu
 int patchify(const float* img, void* out, int B, int S, int P, int Kp, int dtype, cudaStream_t s);
@@ -124,6 +136,15 @@ int match(const float* metric, const void* qkv, int qkv_dtype, int B, int t, int
 size_t match_tc_scratch_bytes(int B, int c);
 int match_tc(const float* metric, const void* qkv, int qkv_dtype, int B, int t, int heads, int c,
              int r, int32_t* src, int32_t* dst, int32_t* unm, float* scratch, cudaStream_t s);
+// Fused merge (bf16 path): merge_map turns a layer's (src, unm) into the per-row destination map
+// of EPI_BIAS_RESID_MERGE; merge_fixup, after that GEMM, computes the size-weighted rows of the
+// destination tokens that received sources (and their bf16 copy / row statistics) and the new
+// size vector.
+int merge_map(const int32_t* src, const int32_t* unm, int B, int t, int r, int32_t* row_map,
+              cudaStream_t s);
+int merge_fixup(float* x_out, const float* side, const float* size, float* size_out, int B, int t,
+                int D, int r, const int32_t* src, const int32_t* dst, const int32_t* unm, void* xh,
+                float* stats, cudaStream_t s);
 int merge(const float* x, const float* size, int B, int t, int D, int r, const int32_t* src,
           const int32_t* dst, const int32_t* unm, const float* ln_w, const float* ln_b,
           float* x_out, float* size_out, void* h_out, int h_dtype, cudaStream_t s,

@@ -39,6 +39,21 @@ int device_sm_count() {
   return count;
 }
 
+// Fused proj + merge on the bf16 LN-folded path (TA_MERGE_FUSION=1; off by default): the proj
+// GEMM writes rows to their merged positions plus their bf16 copy / statistics, merge_fixup
+// finishes the destination rows.  Measured a wash against proj + merge_kernel (ViT-B/16 b=256
+// gamma=-16, ncu launch lists: 5473 vs 5466 us per forward; the epilogue's bf16-copy / statistics
+// writes cost the proj GEMM as much as the merge kernel they replace), so the separate merge
+// kernel stays the default.
+int merge_fusion_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* v = getenv("TA_MERGE_FUSION");
+    on = (v && v[0] == '1') ? 1 : 0;
+  }
+  return on;
+}
+
 int pdl_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -141,6 +156,8 @@ struct Workspace {
   int32_t* unm;
   float* match_scratch;
   float* stats[2];  // LN-folded path: per-row (sum, sumsq) for LN1 / LN2
+  int32_t* row_map;  // fused merge: destination of every input row (merge_map)
+  float* side;       // fused merge: the merged-away source rows [B, r_max, D]
   size_t total;
 };
 
@@ -170,6 +187,10 @@ Workspace carve(const ta_model* m, int B, const Schedule& s, char* base) {
   // LN-folded path: per-row partial (sum, sumsq) per 128-column block (GemmEpi::stats)
   w.stats[0] = reinterpret_cast<float*>(take(rows * 8 * (D / 128)));
   w.stats[1] = reinterpret_cast<float*>(take(rows * 8 * (D / 128)));
+  int r_max = 0;
+  for (int r : s.r) r_max = std::max(r_max, r);
+  w.row_map = reinterpret_cast<int32_t*>(take(r_max > 0 ? rows * 4 : 0));
+  w.side = reinterpret_cast<float*>(take(static_cast<size_t>(B) * r_max * D * 4));
   w.total = off;
   return w;
 }
@@ -508,15 +529,51 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
       prof.mark(TA_STAGE_QKV, l);
       }
     }
+    const int r = s.r[l];
+    // Merge-layer indices (ToMe match on this layer's keys): the match needs only qkv, so with
+    // the fused merge it runs before attention and the proj GEMM moves rows to their merged
+    // positions itself (EPI_BIAS_RESID_MERGE); otherwise the classic order proj -> match -> merge.
+    int32_t *src = w.src, *dst = w.dst, *unm = w.unm;
+    const bool fuse_merge = r > 0 && fused && merge_fusion_enabled() && gemm_pair_path(M, D);
+    auto do_match = [&]() -> int {
+      const int na = (t + 1) / 2;
+      const int32_t* base = forced_trace ? forced_trace : merge_trace;
+      if (base) {
+        src = const_cast<int32_t*>(base) + trace_off;
+        dst = src + static_cast<size_t>(B) * r;
+        unm = dst + static_cast<size_t>(B) * r;
+      }
+      trace_off += static_cast<size_t>(B) * (2 * r + na - r);
+      if (!forced_trace)
+        return match(nullptr, w.qkv, act, B, t, d.heads, m->hd, r, src, dst, unm, w.match_scratch, st);
+      if (merge_trace)
+        cudaMemcpyAsync(merge_trace + (src - forced_trace), src,
+                        sizeof(int32_t) * static_cast<size_t>(B) * (2 * r + na - r),
+                        cudaMemcpyDeviceToDevice, st);
+      return TA_OK;
+    };
+    if (fuse_merge) {
+      TA_TRY(do_match());
+      TA_TRY(merge_map(src, unm, B, t, r, w.row_map, st));
+      prof.mark(TA_STAGE_MATCH, l);
+    }
     TA_TRY(attention(w.qkv, size, B, t, d.heads, m->hd, w.attn, act, st));
       prof.mark(TA_STAGE_ATTENTION, l);
-    const int r = s.r[l];
-    {  // proj + residual (+ LN2 stats when no merge follows)
+    {  // proj + residual (+ LN2 stats when no merge follows; + the merge's row movement)
       GemmEpi e;
       e.bias = static_cast<const float*>(Lw.proj_b);
       e.resid = w.x[cur];
       e.out = w.x[cur];
-      if (fused && r == 0) {
+      if (fuse_merge) {
+        e.out = w.x[cur ^ 1];
+        e.xh = w.h;
+        e.stats = ln2_stats;
+        e.stat_slots = stat_slots;
+        e.row_map = w.row_map;
+        e.side = w.side;
+        TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID_MERGE, e, st));
+      prof.mark(TA_STAGE_PROJ, l);
+      } else if (fused && r == 0) {
         e.xh = w.h;
         e.stats = ln2_stats;
         e.stat_slots = stat_slots;
@@ -529,26 +586,16 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
     }
     int tp = t;
     if (r > 0) {
-      const int na = (t + 1) / 2;
-      int32_t *src = w.src, *dst = w.dst, *unm = w.unm;
-      const int32_t* base = forced_trace ? forced_trace : merge_trace;
-      if (base) {
-        src = const_cast<int32_t*>(base) + trace_off;
-        dst = src + static_cast<size_t>(B) * r;
-        unm = dst + static_cast<size_t>(B) * r;
+      if (fuse_merge) {
+        TA_TRY(merge_fixup(w.x[cur ^ 1], w.side, size, w.size[size_buf], B, t, D, r, src, dst, unm, w.h,
+                           ln2_stats, st));
+      } else {
+        TA_TRY(do_match());
+        prof.mark(TA_STAGE_MATCH, l);
+        TA_TRY(merge(w.x[cur], size, B, t, D, r, src, dst, unm, static_cast<const float*>(Lw.ln2_w),
+                     static_cast<const float*>(Lw.ln2_b), w.x[cur ^ 1], w.size[size_buf], w.h, act,
+                     st, fused ? ln2_stats : nullptr));
       }
-      trace_off += static_cast<size_t>(B) * (2 * r + na - r);
-      if (!forced_trace)
-        TA_TRY(match(nullptr, w.qkv, act, B, t, d.heads, m->hd, r, src, dst, unm, w.match_scratch,
-                     st));
-      else if (merge_trace)
-        cudaMemcpyAsync(merge_trace + (src - forced_trace), src,
-                        sizeof(int32_t) * static_cast<size_t>(B) * (2 * r + na - r),
-                        cudaMemcpyDeviceToDevice, st);
-      prof.mark(TA_STAGE_MATCH, l);
-      TA_TRY(merge(w.x[cur], size, B, t, D, r, src, dst, unm, static_cast<const float*>(Lw.ln2_w),
-                   static_cast<const float*>(Lw.ln2_b), w.x[cur ^ 1], w.size[size_buf], w.h, act,
-                   st, fused ? ln2_stats : nullptr));
       prof.mark(TA_STAGE_MERGE, l);
       cur ^= 1;
       size = w.size[size_buf];

@@ -595,6 +595,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           const long long bm = m / epi.rows_in;
           orow = bm * epi.rows_out + epi.row_off + (m - bm * epi.rows_in);
         }
+        constexpr bool kMerge = EPI == EPI_BIAS_RESID_MERGE;
+        if constexpr (kMerge) orow = row_ok ? __ldg(epi.row_map + m) : 0;
+        // rows that get a bf16 copy and statistics: every valid row, except merged-away sources
+        const bool keep_row = row_ok && (!kMerge || orow >= 0);
         // compute(c): TMEM columns of box c -> bias / LN / GELU / residual -> 8 packed 16-byte
         // words of this thread's row (w); stage_store(c, w): swizzled staging box + TMA store.
         auto compute = [&](int c, uint4 (&w)[8]) -> bool {
@@ -674,7 +678,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           }
           if constexpr (epi_is_stats(EPI)) {
             // bf16 copy of the stored row chunk (next GEMM's A operand) + row statistics
-            if (row_ok) {
+            if (keep_row) {
               uint4* xr = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.xh) + orow * N + n0);
               static_assert(CW % 16 == 0, "32-byte xh stores");
 #pragma unroll
@@ -756,7 +760,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
         auto direct_store = [&](int c, const uint4 (&w)[8]) {
           if (!row_ok || epi.skip == 2) return;
           const int n0 = n_blk * BN + col0 + c * CW;
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<OutT*>(epi.out) + m * N + n0);
+          OutT* row_ptr = static_cast<OutT*>(epi.out) + m * N;
+          if constexpr (kMerge)  // x' row, or the side row of a merged-away source token
+            row_ptr = orow >= 0 ? static_cast<OutT*>(epi.out) + orow * N
+                                : reinterpret_cast<OutT*>(epi.side) + (-1 - orow) * N;
+          uint4* dst = reinterpret_cast<uint4*>(row_ptr + n0);
 #pragma unroll
           for (int j = 0; j < 4; ++j) stg256(dst + 2 * j, w[2 * j], w[2 * j + 1]);
         };
@@ -764,7 +772,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
         for (int c = 0; c < NCH; ++c) {
           uint4 w[8];
           if (compute(c, w)) {
-            if (!kRemap && epi.direct_store)
+            if (kMerge || (!kRemap && epi.direct_store))
               direct_store(c, w);
             else
               stage_store(c, w);
@@ -772,7 +780,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
         }
         if constexpr (epi_is_stats(EPI)) {
           static_assert(BN / kSplit == 128, "one stats slot per warp and tile");
-          if (row_ok && !epi.skip)
+          if (keep_row && !epi.skip)
             *reinterpret_cast<float2*>(epi.stats + 2 * (orow * epi.stat_slots + (n_blk * BN + col0) / 128)) =
                 make_float2(st_s, st_q);
         }
@@ -1037,7 +1045,7 @@ static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
     attr_done(attr_mask);
   }
   CUtensorMap tc_{};
-  if (Cfg::kTma) {
+  if (Cfg::kTma && EPI != EPI_BIAS_RESID_MERGE) {  // the merge kind stores rows directly
     const int rc = kRemap ? make_tmap_out3(&tc_, epi.out, M / epi.rows_in, epi.rows_out, N, sizeof(OutT) == 2)
                           : make_tmap_out(&tc_, epi.out, M, N, sizeof(OutT) == 2);
     if (rc) return rc;
@@ -1081,6 +1089,8 @@ static int dispatch_pair(const CUtensorMap& a, const CUtensorMap& b, int M, int 
       return launch_pair<EPI_LN_BIAS, __nv_bfloat16>(a, b, M, N, K, epi, s);
     case EPI_LN_GELU:
       return launch_pair<EPI_LN_GELU, __nv_bfloat16>(a, b, M, N, K, epi, s);
+    case EPI_BIAS_RESID_MERGE:
+      return launch_pair<EPI_BIAS_RESID_MERGE, float, false>(a, b, M, N, K, epi, s);
   }
   return TA_ERR_INVALID;
 }
@@ -1150,6 +1160,7 @@ int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, b
   // 14.8 us, fc2 18.1 vs 25.4 us at M = 2816); everywhere else the pair kernel wins.
   const bool tiny = M <= 3072 && N <= 1024;
   const int BN = (force_bn == 128 || tiny) ? 128 : (N % 256 == 0) ? 256 : 128;
+  if (epi_kind == EPI_BIAS_RESID_MERGE && !(BN == 256 && gemm_backend() == 0)) return TA_ERR_SHAPE;
   CUtensorMap ta_, tb_;
   int rc = make_tmap_bf16_2d(&ta_, A, M, K, kBM);
   if (rc) return rc;
@@ -1162,6 +1173,13 @@ int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, b
   if (rc) return rc;
   return BN == 256 ? dispatch_bf16<256>(ta_, tb_, M, N, K, epi_kind, out_bf16, epi, stream)
                    : dispatch_bf16<128>(ta_, tb_, M, N, K, epi_kind, out_bf16, epi, stream);
+}
+
+bool gemm_pair_path(int M, int N) {
+  const char* v = getenv("TA_GEMM_BN");
+  const bool force128 = v && atoi(v) == 128;
+  const bool tiny = M <= 3072 && N <= 1024;
+  return !force128 && !tiny && N % 256 == 0 && gemm_backend() == 0;
 }
 
 int gemm_f32(const float* A, const float* W, int M, int N, int K, int epi_kind,

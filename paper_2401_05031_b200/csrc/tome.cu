@@ -340,6 +340,166 @@ static int merge_dispatch(const float* x, const float* size, int B, int t, int D
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 
+// ------------------------------------------------------------------ fused merge (bf16 path)
+// merge_map: per input row of a layer, where the proj GEMM (EPI_BIAS_RESID_MERGE) writes it:
+// unmerged A token -> its position in x' (ToMe output order [A_unm ; B]), B token -> its
+// position after the unmerged A tokens, merged-away A token (src rank k) -> side row b r + k.
+__global__ void __launch_bounds__(256) merge_map_kernel(const int32_t* __restrict__ src,
+                                                        const int32_t* __restrict__ unm, int t, int r,
+                                                        int32_t* __restrict__ row_map) {
+  const int b = blockIdx.x;
+  const int na = (t + 1) / 2, nb = t / 2, n_unm = na - r, tp = t - r;
+  const long long in0 = static_cast<long long>(b) * t;
+  const int out0 = b * tp;
+  grid_dep_wait();
+  grid_dep_launch();
+  for (int p = threadIdx.x; p < n_unm; p += blockDim.x)
+    row_map[in0 + 2 * unm[static_cast<long long>(b) * n_unm + p]] = out0 + p;
+  for (int k = threadIdx.x; k < r; k += blockDim.x)
+    row_map[in0 + 2 * src[static_cast<long long>(b) * r + k]] = -1 - (b * r + k);
+  for (int j = threadIdx.x; j < nb; j += blockDim.x) row_map[in0 + 2 * j + 1] = out0 + n_unm + j;
+}
+
+// merge_fixup: x' already holds every kept token's row (written by the proj GEMM) and `side`
+// the merged-away sources.  Each destination B token that received sources becomes
+// (s_d x_d + sum_k s_k x_k) / (s_d + sum_k s_k) in merge_kernel's order (self, then sources by
+// rank), with its bf16 copy and whole-row statistics (slot 0); block y == 0 also writes the new
+// size vector (ToMe merge_wavg's size sum).  One warp per destination (at its first source).
+template <int VEC>
+__global__ void __launch_bounds__(256)
+    merge_fixup_kernel(float* __restrict__ x_out, const float* __restrict__ side,
+                       const float* __restrict__ size, float* __restrict__ size_out, int t, int r,
+                       const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                       const int32_t* __restrict__ unm, __nv_bfloat16* __restrict__ xh,
+                       float* __restrict__ stats) {
+  constexpr int D = 128 * VEC;
+  constexpr int kMaxT = 1024;
+  __shared__ int s_src[256];
+  __shared__ int s_dst[256];
+  __shared__ float s_size[kMaxT];  // this image's token sizes (ones at the first merge layer)
+  const int b = blockIdx.x;
+  const int na = (t + 1) / 2, n_unm = na - r, tp = t - r;
+  grid_dep_wait();
+  grid_dep_launch();
+  // every global read up front and coalesced: the size loop below is then shared-memory only
+  for (int i = threadIdx.x; i < r; i += blockDim.x) {
+    s_src[i] = src[static_cast<long long>(b) * r + i];
+    s_dst[i] = dst[static_cast<long long>(b) * r + i];
+  }
+  for (int i = threadIdx.x; i < t; i += blockDim.x)
+    s_size[i] = size != nullptr ? size[static_cast<long long>(b) * t + i] : 1.0f;
+  __syncthreads();
+  if (blockIdx.y == 0) {
+    for (int o = threadIdx.x; o < tp; o += blockDim.x) {
+      float stot;
+      if (o < n_unm) {
+        stot = s_size[2 * unm[static_cast<long long>(b) * n_unm + o]];
+      } else {
+        const int j = o - n_unm;
+        stot = s_size[2 * j + 1];
+        for (int q = 0; q < r; ++q)
+          if (s_dst[q] == j) stot += s_size[2 * s_src[q]];
+      }
+      size_out[static_cast<long long>(b) * tp + o] = stot;
+    }
+  }
+  const int k = blockIdx.y * (blockDim.x / 32) + warp_id();
+  if (k >= r) return;
+  const int j = s_dst[k];
+  for (int q = 0; q < k; ++q)
+    if (s_dst[q] == j) return;  // handled by the warp of its first source
+  const int lane = lane_id();
+  const long long orow = static_cast<long long>(b) * tp + n_unm + j;
+  const float s = s_size[2 * j + 1];
+  float4* xr = reinterpret_cast<float4*>(x_out + orow * D);
+  float4 acc[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const float4 v = xr[lane + 32 * i];
+    acc[i] = make_float4(v.x * s, v.y * s, v.z * s, v.w * s);
+  }
+  float stot = s;
+  for (int q = k; q < r; ++q) {
+    if (s_dst[q] != j) continue;
+    const float ss = s_size[2 * s_src[q]];
+    const float4* sr = reinterpret_cast<const float4*>(side + (static_cast<long long>(b) * r + q) * D);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      const float4 v = sr[lane + 32 * i];
+      acc[i].x += v.x * ss;
+      acc[i].y += v.y * ss;
+      acc[i].z += v.z * ss;
+      acc[i].w += v.w * ss;
+    }
+    stot += ss;
+  }
+  float sum = 0.f, q2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    acc[i].x /= stot;
+    acc[i].y /= stot;
+    acc[i].z /= stot;
+    acc[i].w /= stot;
+    sum += (acc[i].x + acc[i].y) + (acc[i].z + acc[i].w);
+    q2 += (acc[i].x * acc[i].x + acc[i].y * acc[i].y) + (acc[i].z * acc[i].z + acc[i].w * acc[i].w);
+    xr[lane + 32 * i] = acc[i];
+    uint2 p;
+    p.x = pack_bf16(acc[i].x, acc[i].y);
+    p.y = pack_bf16(acc[i].z, acc[i].w);
+    *reinterpret_cast<uint2*>(xh + orow * D + 4 * (lane + 32 * i)) = p;
+  }
+  const float s_all = warp_sum(sum), q_all = warp_sum(q2);
+  if (lane < VEC)  // whole-row sums in slot 0, the other 128-column slots zero
+    *reinterpret_cast<float2*>(stats + 2 * (orow * VEC + lane)) =
+        lane == 0 ? make_float2(s_all, q_all) : make_float2(0.f, 0.f);
+}
+
+static cudaLaunchConfig_t pdl_cfg(dim3 grid, cudaStream_t s, cudaLaunchAttribute* attr) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
+int merge_map(const int32_t* src, const int32_t* unm, int B, int t, int r, int32_t* row_map,
+              cudaStream_t s) {
+  if (r <= 0 || r > (t + 1) / 2 - 1) return TA_ERR_INVALID;
+  cudaLaunchAttribute attr[1];
+  const cudaLaunchConfig_t cfg = pdl_cfg(dim3(B), s, attr);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, merge_map_kernel, src, unm, t, r, row_map);
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
+int merge_fixup(float* x_out, const float* side, const float* size, float* size_out, int B, int t,
+                int D, int r, const int32_t* src, const int32_t* dst, const int32_t* unm, void* xh,
+                float* stats, cudaStream_t s) {
+  if (r <= 0 || r > (t + 1) / 2 - 1 || r > 256 || t > 1024) return TA_ERR_INVALID;
+  cudaLaunchAttribute attr[1];
+  const cudaLaunchConfig_t cfg = pdl_cfg(dim3(B, (r + 7) / 8), s, attr);
+  auto* h = static_cast<__nv_bfloat16*>(xh);
+  cudaError_t e;
+  switch (D) {
+#define TA_FIXUP_CASE(DIM, V)                                                                   \
+  case DIM:                                                                                     \
+    e = cudaLaunchKernelEx(&cfg, merge_fixup_kernel<V>, x_out, side, size, size_out, t, r, src, \
+                           dst, unm, h, stats);                                                 \
+    break;
+    TA_FIXUP_CASE(256, 2)
+    TA_FIXUP_CASE(768, 6)
+    TA_FIXUP_CASE(1024, 8)
+    TA_FIXUP_CASE(1280, 10)
+#undef TA_FIXUP_CASE
+    default:
+      return TA_ERR_SHAPE;
+  }
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
 int merge(const float* x, const float* size, int B, int t, int D, int r, const int32_t* src,
           const int32_t* dst, const int32_t* unm, const float* ln_w, const float* ln_b,
           float* x_out, float* size_out, void* h_out, int h_dtype, cudaStream_t s,

@@ -185,3 +185,26 @@ def test_ln_fold_outlier_channels(gamma):
     helpers.record("ln_fold_outliers", {"gamma": gamma, "err_fold": errs[True], "err_nofold": errs[False],
                                         "max_logit": scale})
     assert errs[True] <= 2.0 * errs[False] + 0.25 * BF16_TOL * scale, errs
+
+
+def test_merge_fusion_matches_merge_kernel(tmp_path):
+    """The optional fused proj + merge path (TA_MERGE_FUSION=1) gives the same merge decisions
+    and, with the same forced trace, logits within the bf16 bound of the default path."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    for flag in ("0", "1"):
+        env = dict(os.environ, TA_MERGE_FUSION=flag)
+        r = subprocess.run([sys.executable, os.path.join(here, "merge_fusion_check.py"), str(tmp_path)],
+                           env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+    for gamma in (-16, -8):
+        a = torch.load(tmp_path / f"fusion0_g{gamma}.pt")
+        b = torch.load(tmp_path / f"fusion1_g{gamma}.pt")
+        fa, fb = _finite(a["forced"]), _finite(b["forced"])
+        scale = fa.abs().max().item()
+        assert (fa - fb).abs().max().item() <= BF16_TOL * scale
+        # free-running: identical up to the first layer whose decisions differ on a near-tie
+        assert (a["trace"] == b["trace"]).float().mean().item() > 0.9

@@ -15,14 +15,29 @@ cap() {  # name gamma regex skip
   timeout 300 $NCU --set full --import-source on -k "regex:$3" -s $4 -c 1 -o $OUT/prof_${TAG}_$1 -f \
     python tools/launch_list.py $2 > /dev/null 2>&1
 }
-cap fc1_inforward 0 'pair_kernel<7' 2      # fc1 + LN-fold + GELU, layer 2, t=197
-cap qkv_inforward 0 'pair_kernel<6' 2      # QKV + LN-fold
-cap fc2_inforward 0 'pair_kernel<4' 5      # fc2 + residual + stats (odd launches of kind 4 are fc2 at gamma 0)
-cap proj_inforward 0 'pair_kernel<4' 4     # proj + residual + stats
-cap proj_merge_inforward -8 'pair_kernel<2' 2  # proj + residual before a merge
+# demangled names read "gemm_bf16_sm100_pair_kernel<(int)7, ...>"; pair-kernel launch order at
+# gamma 0: patch (kind 5), then per layer qkv (6), proj (4), fc1 (7), fc2 (4)
+cap fc1_inforward 0 'pair_kernel<\(int\)7' 2      # fc1 + LN-fold + GELU, layer 2, t=197
+cap qkv_inforward 0 'pair_kernel<\(int\)6' 2      # QKV + LN-fold
+cap fc2_inforward 0 'pair_kernel<\(int\)4' 5      # fc2 + residual + stats (odd kind-4 launches at gamma 0)
+cap proj_inforward 0 'pair_kernel<\(int\)4' 4     # proj + residual + stats
+cap proj_merge_inforward -8 'pair_kernel<\(int\)2' 2  # proj + residual before a merge
 cap attn_t197_inforward 0 'attn_tc_kernel' 2
 cap attn_t389_inforward 16 'attn_tc_kernel' 11
 cap match_bf16_inforward -8 'match_fused_kernel' 2
 cap merge_inforward -8 'merge_kernel' 2
 cap patchify_inforward 0 'patchify' 0
+cap head_inforward 0 'head_kernel' 0
 ls -la $OUT | grep prof_${TAG}
+# summaries on the box (gpurun_out is capped at 64 MiB on the way back)
+mkdir -p $OUT/prof_${TAG}_txt
+PROFILE_DST=$OUT/prof_${TAG}_txt python tools/summarize_profiles.py $TAG > /dev/null 2>&1
+for r in $OUT/prof_${TAG}_*.ncu-rep; do
+  python tools/ncu_stalls.py $r 30 > $OUT/prof_${TAG}_txt/stalls_$(basename $r .ncu-rep).txt 2>&1
+done
+mkdir -p $OUT/prof_${TAG}_keep
+for k in fc1_inforward qkv_inforward fc2_inforward attn_t197_inforward; do
+  mv $OUT/prof_${TAG}_$k.ncu-rep $OUT/prof_${TAG}_keep/ 2>/dev/null
+done
+rm -f $OUT/prof_${TAG}_*.ncu-rep
+du -sh $OUT
