@@ -114,6 +114,13 @@ int gemm_f32(const float* A, const float* W, int M, int N, int K, int epi_kind,
              const GemmEpi& epi, cudaStream_t stream);
 // Whether gemm_bf16 runs (M, N) on the CTA-pair kernel (the only one with EPI_BIAS_RESID_MERGE).
 bool gemm_pair_path(int M, int N);
+// fp32 parity mode on the tensor cores: 3xTF32 tcgen05 GEMM (kind::tf32, operands split into
+// tf32 hi + lo in `scratch`, gemm_f32_tc_scratch_bytes(M, N, K)); f32_gemm_backend() == 1 when
+// TA_F32_GEMM=simt selects the SIMT FFMA kernel instead.
+size_t gemm_f32_tc_scratch_bytes(int M, int N, int K);
+int gemm_f32_tc(const float* A, const float* W, int M, int N, int K, int epi_kind, const GemmEpi& epi,
+                void* scratch, cudaStream_t stream);
+int f32_gemm_backend();
 
 // rowops.cu
 int patchify(const float* img, void* out, int B, int S, int P, int Kp, int dtype, cudaStream_t s);

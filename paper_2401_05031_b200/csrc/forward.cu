@@ -156,6 +156,7 @@ struct Workspace {
   int32_t* unm;
   float* match_scratch;
   float* stats[2];  // LN-folded path: per-row (sum, sumsq) for LN1 / LN2
+  void* tf32_scratch;  // fp32 mode: tf32 hi / lo operand split of the 3xTF32 GEMMs
   int32_t* row_map;  // fused merge: destination of every input row (merge_map)
   float* side;       // fused merge: the merged-away source rows [B, r_max, D]
   size_t total;
@@ -189,6 +190,11 @@ Workspace carve(const ta_model* m, int B, const Schedule& s, char* base) {
   w.stats[1] = reinterpret_cast<float*>(take(rows * 8 * (D / 128)));
   int r_max = 0;
   for (int r : s.r) r_max = std::max(r_max, r);
+  // fp32 mode: the largest GEMM operand pair (rows x MLP for fc2's A, MLP x D for its W)
+  w.tf32_scratch = take(m->d.dtype == TA_DTYPE_F32
+                            ? gemm_f32_tc_scratch_bytes(static_cast<int>(rows), m->d.mlp_dim,
+                                                        std::max(m->d.mlp_dim, m->kp))
+                            : 0);
   w.row_map = reinterpret_cast<int32_t*>(take(r_max > 0 ? rows * 4 : 0));
   w.side = reinterpret_cast<float*>(take(static_cast<size_t>(B) * r_max * D * 4));
   w.total = off;
@@ -196,10 +202,13 @@ Workspace carve(const ta_model* m, int B, const Schedule& s, char* base) {
 }
 
 int linear(const ta_model* m, const void* a, const void* wt, int M, int N, int K, int epi_kind,
-           const GemmEpi& epi, cudaStream_t st) {
+           const GemmEpi& epi, cudaStream_t st, void* tf32_scratch) {
   if (m->d.dtype == TA_DTYPE_BF16)
     return gemm_bf16(a, wt, M, N, K, epi_kind, epi_kind == EPI_BIAS || epi_kind == EPI_BIAS_GELU || epi_is_ln(epi_kind),
                      epi, st);
+  if (f32_gemm_backend() == 0)
+    return gemm_f32_tc(static_cast<const float*>(a), static_cast<const float*>(wt), M, N, K, epi_kind, epi,
+                       tf32_scratch, st);
   return gemm_f32(static_cast<const float*>(a), static_cast<const float*>(wt), M, N, K, epi_kind,
                   epi, st);
 }
@@ -486,7 +495,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
       e.stat_slots = stat_slots;
     }
     TA_TRY(linear(m, w.patches, m->w.patch_w, B * m->n_patches, D, m->kp,
-                  fused ? EPI_PATCH_STATS : EPI_PATCH, e, st));
+                  fused ? EPI_PATCH_STATS : EPI_PATCH, e, st, w.tf32_scratch));
     prof.mark(TA_STAGE_PATCH_GEMM, -1);
   }
   TA_TRY(insert_rows(w.x[0], B, s.t[0], D, static_cast<const float*>(m->w.cls),
@@ -518,14 +527,14 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         e.c1 = static_cast<const float*>(Lw.qkv_c1);
         e.c2 = static_cast<const float*>(Lw.qkv_c2);
         e.inv_dim = 1.0f / D;
-        TA_TRY(linear(m, w.h, Lw.qkv_w_ln, M, 3 * D, D, EPI_LN_BIAS, e, st));
+        TA_TRY(linear(m, w.h, Lw.qkv_w_ln, M, 3 * D, D, EPI_LN_BIAS, e, st, w.tf32_scratch));
       prof.mark(TA_STAGE_QKV, l);
       } else {
         TA_TRY(layernorm(w.x[cur], static_cast<const float*>(Lw.ln1_w),
                          static_cast<const float*>(Lw.ln1_b), w.h, M, D, act, st));
       prof.mark(TA_STAGE_LN1, l);
         e.bias = static_cast<const float*>(Lw.qkv_b);
-        TA_TRY(linear(m, w.h, Lw.qkv_w, M, 3 * D, D, EPI_BIAS, e, st));
+        TA_TRY(linear(m, w.h, Lw.qkv_w, M, 3 * D, D, EPI_BIAS, e, st, w.tf32_scratch));
       prof.mark(TA_STAGE_QKV, l);
       }
     }
@@ -571,16 +580,16 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         e.stat_slots = stat_slots;
         e.row_map = w.row_map;
         e.side = w.side;
-        TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID_MERGE, e, st));
+        TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID_MERGE, e, st, w.tf32_scratch));
       prof.mark(TA_STAGE_PROJ, l);
       } else if (fused && r == 0) {
         e.xh = w.h;
         e.stats = ln2_stats;
         e.stat_slots = stat_slots;
-        TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID_STATS, e, st));
+        TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID_STATS, e, st, w.tf32_scratch));
       prof.mark(TA_STAGE_PROJ, l);
       } else {
-        TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID, e, st));
+        TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID, e, st, w.tf32_scratch));
       prof.mark(TA_STAGE_PROJ, l);
       }
     }
@@ -616,11 +625,11 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         e.c1 = static_cast<const float*>(Lw.fc1_c1);
         e.c2 = static_cast<const float*>(Lw.fc1_c2);
         e.inv_dim = 1.0f / D;
-        TA_TRY(linear(m, w.h, Lw.fc1_w_ln, Mp, d.mlp_dim, D, EPI_LN_GELU, e, st));
+        TA_TRY(linear(m, w.h, Lw.fc1_w_ln, Mp, d.mlp_dim, D, EPI_LN_GELU, e, st, w.tf32_scratch));
       prof.mark(TA_STAGE_FC1, l);
       } else {
         e.bias = static_cast<const float*>(Lw.fc1_b);
-        TA_TRY(linear(m, w.h, Lw.fc1_w, Mp, d.mlp_dim, D, EPI_BIAS_GELU, e, st));
+        TA_TRY(linear(m, w.h, Lw.fc1_w, Mp, d.mlp_dim, D, EPI_BIAS_GELU, e, st, w.tf32_scratch));
       prof.mark(TA_STAGE_FC1, l);
       }
     }
@@ -645,7 +654,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         e.stat_slots = stat_slots;
       }
       TA_TRY(linear(m, w.mlp, Lw.fc2_w, Mp, D, d.mlp_dim,
-                    stats ? EPI_BIAS_RESID_STATS : EPI_BIAS_RESID, e, st));
+                    stats ? EPI_BIAS_RESID_STATS : EPI_BIAS_RESID, e, st, w.tf32_scratch));
       prof.mark(TA_STAGE_FC2, l);
       if (restride) cur ^= 1;
     }
@@ -763,6 +772,16 @@ int ta_gemm(const void* a, const void* w, const float* bias, const float* resid,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (dtype == TA_DTYPE_BF16) return gemm_bf16(a, w, m, n, k, epilogue, out_dtype == TA_DTYPE_BF16, e, st);
   if (out_dtype != TA_DTYPE_F32) return TA_ERR_INVALID;
+  if (f32_gemm_backend() == 0 && k % 32 == 0 && n % 128 == 0) {
+    // unit entry point: stream-ordered scratch for the tf32 operand split
+    void* scratch = nullptr;
+    cudaError_t ce = cudaMallocAsync(&scratch, gemm_f32_tc_scratch_bytes(m, n, k), st);
+    if (ce != cudaSuccess) return set_last_cuda_error(ce);
+    const int rc = gemm_f32_tc(static_cast<const float*>(a), static_cast<const float*>(w), m, n, k, epilogue,
+                               e, scratch, st);
+    cudaFreeAsync(scratch, st);
+    return rc;
+  }
   return gemm_f32(static_cast<const float*>(a), static_cast<const float*>(w), m, n, k, epilogue, e, st);
 }
 

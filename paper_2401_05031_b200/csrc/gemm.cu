@@ -23,6 +23,12 @@
 
 namespace ta {
 
+#define TA_TRY_GEMM(expr)     \
+  do {                        \
+    const int rc_ = (expr);   \
+    if (rc_ != TA_OK) return rc_; \
+  } while (0)
+
 // ------------------------------------------------------------------ epilogue
 // One epilogue warp owns TMEM lanes [32*q, 32*q + 32) (q = warp % 4) and a 128-column
 // half of the 256-wide accumulator.  Per 32-column chunk: tcgen05.ld (thread = row) ->
@@ -208,23 +214,38 @@ __host__ __device__ constexpr int pair_epi_warps(int e, bool remap) {
   return pair_tma(e, remap) ? 8 : epi_warps(e);
 }
 
-template <int BN>
+// kOp 0: bf16 operands (64 K per 128-byte row).  kOp 1: fp32 parity mode on the tensor cores,
+// 3xTF32: every stage holds A_hi, A_lo, W_hi, W_lo (32 fp32 K per 128-byte row; x = hi + lo
+// with hi = x truncated to tf32, split by split_tf32_kernel) and C = A_hi W_hi^T + A_hi W_lo^T
+// + A_lo W_hi^T accumulates in fp32 in TMEM (kind::tf32; the dropped lo*lo term is ~2^-22
+// relative, the same scheme as the fp32 bipartite match in match_tc.cu).
+template <int BN, int kOp = 0>
 struct GemmCfg {
-  static constexpr int kStages = BN == 256 ? 4 : 6;
-  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kParts = kOp ? 2 : 1;  // hi (+ lo) per operand
+  static constexpr int kStages = kOp ? 3 : (BN == 256 ? 4 : 6);
+  static constexpr int kABytes = kBM * kBK * 2;  // one 128 x 128-byte tile
   static constexpr int kBBytes = BN * kBK * 2;
-  static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kTmemCols = 2 * BN;  // two accumulator stages
+  static constexpr int kStageBytes = kParts * (kABytes + kBBytes);
+  static constexpr int kKPerStage = kOp ? kBK / 2 : kBK;  // 32 fp32 or 64 bf16 per 128-byte row
+  // kOp 0: two accumulator stages.  kOp 1: two K-chunk buffers + the running total (below).
+  static constexpr int kTmemCols = kOp ? 512 : 2 * BN;
+  // kOp 1: the tensor core's fp32 accumulation truncates, so its error grows with the number of
+  // MMAs summed into one accumulator (measured ~2e-5 relative at K = 768 in one accumulator).  The
+  // MMAs of every 64-K chunk go into a fresh chunk buffer, and the epilogue warps add the chunks
+  // into a running total in TMEM with round-to-nearest FADDs (error ~24 MMAs' worth per chunk).
+  static constexpr int kChunkKb = 2;  // k-blocks (of 32 fp32) per chunk
   static constexpr int kEpiBytes = kEpiWarps * 32 * 32 * 4;  // per-warp 32x32 fp32 transpose
   static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 256;
 };
 
-template <int BN, int EPI, typename OutT, bool kRemap>
+template <int BN, int EPI, typename OutT, bool kRemap, int kOp = 0>
 __global__ void __launch_bounds__(gemm_threads(EPI), 1)
     gemm_bf16_sm100_kernel(const __grid_constant__ CUtensorMap tmA,
-                           const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                           const __grid_constant__ CUtensorMap tmB,
+                           const __grid_constant__ CUtensorMap tmA2,
+                           const __grid_constant__ CUtensorMap tmB2, int M, int N, int K,
                            GemmEpi epi) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, kOp>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -242,6 +263,10 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if constexpr (kOp) {
+      tma_prefetch(&tmA2);
+      tma_prefetch(&tmB2);
+    }
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < S; ++s) {
@@ -267,7 +292,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
   const int num_m = (M + kBM - 1) / kBM;
   const int num_n = N / BN;
   const int num_tiles = num_m * num_n;
-  const int num_kb = K / kBK;
+  const int num_kb = K / Cfg::kKPerStage;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -281,8 +306,13 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
           uint8_t* sa = smem + stage * Cfg::kStageBytes;
           uint8_t* sb = sa + Cfg::kABytes;
           mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
-          tma_load_2d(&tmA, &full[stage], sa, kb * kBK, m_blk * kBM);
-          tma_load_2d(&tmB, &full[stage], sb, kb * kBK, n_blk * BN);
+          const int kc = kb * Cfg::kKPerStage;
+          tma_load_2d(&tmA, &full[stage], sa, kc, m_blk * kBM);
+          tma_load_2d(&tmB, &full[stage], sb, kc, n_blk * BN);
+          if constexpr (kOp) {  // stage = [A_hi][W_hi][A_lo][W_lo]
+            tma_load_2d(&tmA2, &full[stage], sb + Cfg::kBBytes, kc, m_blk * kBM);
+            tma_load_2d(&tmB2, &full[stage], sb + Cfg::kBBytes + Cfg::kABytes, kc, n_blk * BN);
+          }
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -298,31 +328,63 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        if constexpr (!kOp) {
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
+          tc_fence_after();
+        }
+        uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
+          if constexpr (kOp) {
+            if (kb % Cfg::kChunkKb == 0) {  // a new chunk: wait for its buffer to be drained
+              mbar_wait(&tempty[acc], acc_phase ^ 1);
+              tc_fence_after();
+              d_tmem = tmem_base + acc * BN;
+            }
+          }
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * Cfg::kStageBytes);
           const uint32_t sb = sa + Cfg::kABytes;
           const uint64_t adesc = umma_desc_sw128(sa);
           const uint64_t bdesc = umma_desc_sw128(sb);
+          if constexpr (kOp) {
+            constexpr uint32_t idesc32 = idesc_tf32(kBM, BN);
+            const uint64_t alo = umma_desc_sw128(sb + Cfg::kBBytes);
+            const uint64_t blo = umma_desc_sw128(sb + Cfg::kBBytes + Cfg::kABytes);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            // +32 bytes per K=16 step inside the 128-byte swizzle row (encoded >> 4).
-            umma_f16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < 4; ++k) {  // K = 8 tf32 = 32 bytes per instruction
+              umma_tf32(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc32, ((kb % Cfg::kChunkKb) | k) != 0);
+              umma_tf32(d_tmem, adesc + 2 * k, blo + 2 * k, idesc32, 1);
+              umma_tf32(d_tmem, alo + 2 * k, bdesc + 2 * k, idesc32, 1);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) {
+              // +32 bytes per K=16 step inside the 128-byte swizzle row (encoded >> 4).
+              umma_f16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            }
           }
           umma_commit(&empty[stage]);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
+          if constexpr (kOp) {
+            if (kb % Cfg::kChunkKb == Cfg::kChunkKb - 1 || kb == num_kb - 1) {
+              umma_commit(&tfull[acc]);  // chunk complete
+              if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+              }
+            }
+          }
         }
-        umma_commit(&tfull[acc]);
-        if (++acc == 2) {
-          acc = 0;
-          acc_phase ^= 1;
+        if constexpr (!kOp) {
+          umma_commit(&tfull[acc]);
+          if (++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
         }
       }
     }
@@ -345,9 +407,41 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
         if (m < M)
           prefetch_l2_bulk(epi.resid + m * N + n_blk * BN + col0, BN / 2 * sizeof(float));
       }
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * BN + col0;
+      uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * BN + col0;
+      if constexpr (kOp) {
+        // drain the tile's K-chunks into the running total (TMEM columns [2 BN, 3 BN))
+        const uint32_t t_tot = tmem_base + ((q * 32u) << 16) + 2 * BN + col0;
+        const int n_chunks = (num_kb + Cfg::kChunkKb - 1) / Cfg::kChunkKb;
+        for (int ch = 0; ch < n_chunks; ++ch) {
+          mbar_wait(&tfull[acc], acc_phase);
+          tc_fence_after();
+          const uint32_t t_ch = tmem_base + ((q * 32u) << 16) + acc * BN + col0;
+#pragma unroll 1
+          for (int c = 0; c < BN / kSplit; c += 32) {
+            uint32_t a[32], b[32];
+            tmem_ld_32x32b_x32(t_ch + c, a);
+            if (ch > 0) tmem_ld_32x32b_x32(t_tot + c, b);
+            tmem_ld_wait();
+            if (ch > 0) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) a[j] = __float_as_uint(__uint_as_float(b[j]) + __uint_as_float(a[j]));
+            }
+            tmem_st_32x32b_x32(t_tot + c, a);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);  // chunk buffer free for the next MMAs
+          if (++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
+        }
+        t_row = t_tot;
+      } else {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+      }
       uint32_t r0[32], r1[32];
       EpiChunk ca, cb;
       RowStats rs;
@@ -362,7 +456,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
       for (int c = 0; c < kChunks; c += 2) {
         tmem_ld_32x32b_x32(t_row + (c + 1) * 32, r1);
         tmem_ld_wait();
-        if (c + 2 == kChunks) {
+        if (!kOp && c + 2 == kChunks) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -382,9 +476,13 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
           if ((c + 2) % 4 == 0 && live) rowstats_flush<kRemap>(epi, M, m_base, rs, (nb + (c - 2) * 32) / 128);
         }
       }
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
+      if constexpr (!kOp) {
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      } else {
+        tc_fence_before();  // total read before the next tile's first chunk overwrites it
       }
     }
   }
@@ -392,7 +490,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<GemmCfg<BN>::kTmemCols>(tmem_base);
+    tmem_dealloc<Cfg::kTmemCols>(tmem_base);
   }
 }
 
@@ -954,11 +1052,12 @@ int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_
   return r == CUDA_SUCCESS ? TA_OK : TA_ERR_SHAPE;
 }
 
-template <int BN, int EPI, typename OutT, bool kRemap = false>
+template <int BN, int EPI, typename OutT, bool kRemap = false, int kOp = 0>
 static int launch_bf16(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, int N, int K,
-                       const GemmEpi& epi, cudaStream_t stream) {
-  using Cfg = GemmCfg<BN>;
-  auto kern = gemm_bf16_sm100_kernel<BN, EPI, OutT, kRemap>;
+                       const GemmEpi& epi, cudaStream_t stream, const CUtensorMap* ta2 = nullptr,
+                       const CUtensorMap* tb2 = nullptr) {
+  using Cfg = GemmCfg<BN, kOp>;
+  auto kern = gemm_bf16_sm100_kernel<BN, EPI, OutT, kRemap, kOp>;
   static unsigned long long attr_mask = 0;  // per instantiation and device
   if (attr_needed(attr_mask)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -978,7 +1077,7 @@ static int launch_bf16(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta_, tb_, M, N, K, epi);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta_, tb_, ta2 ? *ta2 : ta_, tb2 ? *tb2 : tb_, M, N, K, epi);
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 
@@ -1173,6 +1272,106 @@ int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, b
   if (rc) return rc;
   return BN == 256 ? dispatch_bf16<256>(ta_, tb_, M, N, K, epi_kind, out_bf16, epi, stream)
                    : dispatch_bf16<128>(ta_, tb_, M, N, K, epi_kind, out_bf16, epi, stream);
+}
+
+// ------------------------------------------------------------------ fp32 mode on the tensor cores
+// x = hi + lo with hi = tf32(x) and lo = tf32(x - hi), both rounded to nearest (cvt.rna), so
+// the tensor core's tf32 read of either is exact and x - hi - lo = O(2^-22 |x|): the operand
+// split of the 3xTF32 GEMM (kOp = 1), one pass over each operand.  (Truncating hi and lo, as
+// the match kernel's normalised metric tolerates, leaves O(2^-20 |x|) and flipped a
+// config-1 merge decision against the fp64 oracle.)
+__device__ __forceinline__ float tf32_rna(float v) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+  return __uint_as_float(r);
+}
+__global__ void __launch_bounds__(256) split_tf32_kernel(const float4* __restrict__ x, float4* __restrict__ hi,
+                                                         float4* __restrict__ lo, long long n4) {
+  grid_dep_wait();
+  grid_dep_launch();
+  auto tr = [](float v) { return tf32_rna(v); };
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const float4 v = x[i];
+    const float4 h = make_float4(tr(v.x), tr(v.y), tr(v.z), tr(v.w));
+    hi[i] = h;
+    lo[i] = make_float4(tr(v.x - h.x), tr(v.y - h.y), tr(v.z - h.z), tr(v.w - h.w));
+  }
+}
+
+static int split_tf32(const float* x, float* hi, float* lo, long long n, cudaStream_t s) {
+  if (n % 4) return TA_ERR_SHAPE;
+  const long long n4 = n / 4;
+  cudaLaunchConfig_t cfg = {};
+  const long long blocks = (n4 + 255) / 256;
+  cfg.gridDim = dim3(static_cast<unsigned>(blocks < 4 * 148 ? blocks : 4 * 148));
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, split_tf32_kernel, reinterpret_cast<const float4*>(x),
+                                           reinterpret_cast<float4*>(hi), reinterpret_cast<float4*>(lo), n4);
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
+static int make_tmap_f32_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                            uint32_t box_rows) {
+  auto enc = get_encode_fn();
+  if (!enc) return TA_ERR_CUDA;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 4};
+  cuuint32_t box[2] = {32, box_rows};  // 32 fp32 = one 128-byte swizzle row
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? TA_OK : TA_ERR_SHAPE;
+}
+
+size_t gemm_f32_tc_scratch_bytes(int M, int N, int K) {
+  return (2ull * M * K + 2ull * N * K) * sizeof(float);
+}
+
+// fp32 mode: 3xTF32 tcgen05 GEMM (TA_F32_GEMM=simt selects the SIMT FFMA kernel instead).
+int f32_gemm_backend() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* v = getenv("TA_F32_GEMM");
+    mode = (v && v[0] == 's') ? 1 : 0;
+  }
+  return mode;
+}
+
+int gemm_f32_tc(const float* A, const float* W, int M, int N, int K, int epi_kind, const GemmEpi& epi,
+                void* scratch, cudaStream_t stream) {
+  if (M <= 0) return TA_OK;
+  if (K % 32 != 0 || N % 128 != 0 || !scratch) return TA_ERR_SHAPE;
+  float* a_hi = static_cast<float*>(scratch);
+  float* a_lo = a_hi + static_cast<size_t>(M) * K;
+  float* w_hi = a_lo + static_cast<size_t>(M) * K;
+  float* w_lo = w_hi + static_cast<size_t>(N) * K;
+  TA_TRY_GEMM(split_tf32(A, a_hi, a_lo, static_cast<long long>(M) * K, stream));
+  TA_TRY_GEMM(split_tf32(W, w_hi, w_lo, static_cast<long long>(N) * K, stream));
+  CUtensorMap ta, tb, ta2, tb2;
+  TA_TRY_GEMM(make_tmap_f32_2d(&ta, a_hi, M, K, kBM));
+  TA_TRY_GEMM(make_tmap_f32_2d(&ta2, a_lo, M, K, kBM));
+  TA_TRY_GEMM(make_tmap_f32_2d(&tb, w_hi, N, K, 128));
+  TA_TRY_GEMM(make_tmap_f32_2d(&tb2, w_lo, N, K, 128));
+  switch (epi_kind) {
+    case EPI_BIAS:
+      return launch_bf16<128, EPI_BIAS, float, false, 1>(ta, tb, M, N, K, epi, stream, &ta2, &tb2);
+    case EPI_BIAS_GELU:
+      return launch_bf16<128, EPI_BIAS_GELU, float, false, 1>(ta, tb, M, N, K, epi, stream, &ta2, &tb2);
+    case EPI_BIAS_RESID:
+      return epi.rows_in ? launch_bf16<128, EPI_BIAS_RESID, float, true, 1>(ta, tb, M, N, K, epi, stream, &ta2, &tb2)
+                         : launch_bf16<128, EPI_BIAS_RESID, float, false, 1>(ta, tb, M, N, K, epi, stream, &ta2, &tb2);
+    case EPI_PATCH:
+      return launch_bf16<128, EPI_PATCH, float, true, 1>(ta, tb, M, N, K, epi, stream, &ta2, &tb2);
+  }
+  return TA_ERR_INVALID;
 }
 
 bool gemm_pair_path(int M, int N) {

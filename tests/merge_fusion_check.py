@@ -20,7 +20,9 @@ for gamma in (-16, -8):
     n = bb.trace_len(B, gamma)
     trace = torch.full((n,), -1, dtype=torch.int32, device="cuda")
     out = bb.forward_raw(imgs, ids, gamma, trace=trace)
-    forced = bb.forward_raw(imgs, ids, gamma, forced_trace=trace.clone())
+    ref_path = os.path.join(sys.argv[1], f"fusion0_g{gamma}.pt")  # the default path's trace, if run
+    shared = torch.load(ref_path)["trace"].cuda() if os.path.exists(ref_path) else trace.clone()
+    forced = bb.forward_raw(imgs, ids, gamma, forced_trace=shared)
     torch.cuda.synchronize()
     torch.save({"out": out.cpu(), "forced": forced.cpu(), "trace": trace.cpu()},
                os.path.join(sys.argv[1], f"fusion{os.environ.get('TA_MERGE_FUSION', '0')}_g{gamma}.pt"))
