@@ -100,10 +100,11 @@ def allocate(batches: Sequence[Batch], now_us: int, cfg: AdapterConfig, table: P
     cell, a state with more utility but a later clock can displace the state that lets a later
     batch meet its deadline, and the plan is then suboptimal (13 of the 200 seeded instances of
     tests/test_serving.py with the literal table, ``allocate_single_state``).  A state is pruned
-    only when another state of the same cell has utility >= and clock <= (floating-point
-    addition is monotone, so no pruned state can lead to a better plan), which makes the
-    result exact.  ``frontier_cap`` bounds a cell (kept states: highest utility first); the
-    cap is never reached at the sizes of the acceptance test (N_B <= 6, N_gamma <= 4).
+    only when another state of the same batch (any column) has utility >= and clock <=
+    (floating-point addition is monotone, so no pruned state can lead to a better plan), which
+    makes the result exact.  ``frontier_cap`` bounds a row's frontier (kept: highest utility
+    first); it is not reached at the sizes of the acceptance test (N_B <= 6, N_gamma <= 4), and
+    the serving engine passes a small cap to bound planning time in real time.
     """
     order = _edf(batches)
     if not order:
@@ -118,17 +119,19 @@ def allocate(batches: Sequence[Batch], now_us: int, cfg: AdapterConfig, table: P
         b = order[bi]
         est = [None] + [estimate_batch(b, cfg.gammas.at_column(l), table) for l in range(1, ng + 1)]
         mem_ok = [True] + [_mem_ok(b, cfg.gammas.at_column(l), mem, table) for l in range(1, ng + 1)]
-        row: List[Tuple[float, float, int, int]] = []
+        # The states of every column of this batch form one frontier: a state's future (what later
+        # batches can still do) depends only on its (utility, clock), not on the column it came
+        # from, so a state dominated by one of another column is dropped too.
+        cand: List[Tuple[float, float, int, int]] = []
         for l in range(ng + 1):
-            cell: List[Tuple[float, float, int, int]] = []
             for pi, (u_prev, c_prev, _, _) in enumerate(prev_states):
                 if l == 0:  # skip: utility and clock carried forward (Alg. 2 lines 14-19)
-                    cell.append((u_prev, c_prev, 0, pi))
+                    cand.append((u_prev, c_prev, 0, pi))
                 else:
                     t_hat, u_hat = est[l]
                     if c_prev + t_hat < b.deadline_us and mem_ok[l]:  # Alg. 2 line 23
-                        cell.append((u_prev + u_hat, c_prev + t_hat, l, pi))
-            row.extend(_pareto(cell, frontier_cap))
+                        cand.append((u_prev + u_hat, c_prev + t_hat, l, pi))
+        row = _pareto(cand, frontier_cap)
         rows.append(row)
         prev_states = row
     # argmax of utility; exact ties -> lexicographically smallest column vector (the oracle's rule)
@@ -149,11 +152,10 @@ def allocate(batches: Sequence[Batch], now_us: int, cfg: AdapterConfig, table: P
 
 
 def _pareto(cell: List[Tuple[float, float, int, int]], cap: int) -> List[Tuple[float, float, int, int]]:
-    """Non-dominated (utility up, clock down) states of one DP cell, in insertion order of the
-    survivors' predecessors (earlier predecessor columns win exact ties, as Alg. 2's strict
-    improvement rule does)."""
+    """Non-dominated (utility up, clock down) states of one DP row; exact ties keep the state
+    with the lower column, then the earlier predecessor (Alg. 2's strict-improvement order)."""
     keep: List[Tuple[float, float, int, int]] = []
-    for st in sorted(cell, key=lambda s: (-s[0], s[1], s[3])):
+    for st in sorted(cell, key=lambda s: (-s[0], s[1], s[2], s[3])):
         if keep and keep[-1][1] <= st[1]:
             continue  # an earlier-kept state has utility >= and clock <=
         keep.append(st)

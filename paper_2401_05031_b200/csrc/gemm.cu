@@ -1257,7 +1257,11 @@ int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, b
   // Tiny M x narrow N (ViT tail layers after merging, e.g. M = 256 x 11, N = 768): the 128 x 128
   // single-CTA kernel fills more SMs than 256 x 256 pair tiles (tools/gemm_small.py: proj 9.5 vs
   // 14.8 us, fc2 18.1 vs 25.4 us at M = 2816); everywhere else the pair kernel wins.
-  const bool tiny = M <= 3072 && N <= 1024;
+  static const int tiny_m = [] {  // profiling: TA_GEMM_TINY_M overrides the small-M threshold
+    const char* v = getenv("TA_GEMM_TINY_M");
+    return v ? atoi(v) : 3072;
+  }();
+  const bool tiny = M <= tiny_m && N <= 1024;
   const int BN = (force_bn == 128 || tiny) ? 128 : (N % 256 == 0) ? 256 : 128;
   if (epi_kind == EPI_BIAS_RESID_MERGE && !(BN == 256 && gemm_backend() == 0)) return TA_ERR_SHAPE;
   CUtensorMap ta_, tb_;
@@ -1377,7 +1381,8 @@ int gemm_f32_tc(const float* A, const float* W, int M, int N, int K, int epi_kin
 bool gemm_pair_path(int M, int N) {
   const char* v = getenv("TA_GEMM_BN");
   const bool force128 = v && atoi(v) == 128;
-  const bool tiny = M <= 3072 && N <= 1024;
+  const char* tv = getenv("TA_GEMM_TINY_M");
+  const bool tiny = M <= (tv ? atoi(tv) : 3072) && N <= 1024;
   return !force128 && !tiny && N % 256 == 0 && gemm_backend() == 0;
 }
 

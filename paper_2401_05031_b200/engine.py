@@ -57,6 +57,11 @@ class EngineConfig:
     policy: object = "otas"
     seed: int = 0
     correctness: str = "sampled"  # or "expected"
+    # Planning cost bounds (real-time serving: the plan is recomputed at every dispatch, on the
+    # host, while the replicas compute): DP over the `dp_horizon` earliest-deadline batches only
+    # (None = the whole queue, Alg. 2 as specified) with `frontier_cap` states per DP row.
+    dp_horizon: Optional[int] = None
+    frontier_cap: int = 256
 
     def __post_init__(self) -> None:
         if not (self.policy == "otas" or isinstance(self.policy, int)):
@@ -300,7 +305,10 @@ class ServingEngine:
 
     def _plan(self, batches: List[Batch], now: int, rate: float, initial: bool) -> TokenPlan:
         if self.cfg.policy == "otas":
-            return allocate(batches, now, self.adapter, self.table, self.mem, rate, initial_stage=initial)
+            if self.cfg.dp_horizon is not None and len(batches) > self.cfg.dp_horizon:
+                batches = sorted(batches, key=lambda b: (b.deadline_us, b.id))[: self.cfg.dp_horizon]
+            return allocate(batches, now, self.adapter, self.table, self.mem, rate, initial_stage=initial,
+                            frontier_cap=self.cfg.frontier_cap)
         return TokenPlan({b.id: self.cfg.policy for b in batches})
 
     def run(self, queries: Sequence[Query]) -> SimReport:
@@ -356,7 +364,7 @@ class ServingEngine:
                 nxt += 1
             rate = arrival_rate(arrivals, now, self.adapter.rate_window_us)
             plan = self._plan(list(queue.batches), now, rate, now - start < self.adapter.initial_stage_us)
-            for b in [b for b in queue.batches if plan.is_skip(b.id)]:
+            for b in [b for b in queue.batches if b.id in plan.assignments and plan.is_skip(b.id)]:
                 queue.remove(b)
                 finalize(b, None, None, r_i, 0)
             if not queue.batches:
@@ -439,7 +447,7 @@ class ServingEngine:
                 while queue.batches and not busy[r]:
                     rate = arrival_rate(arrivals, now, self.adapter.rate_window_us)
                     plan = self._plan(list(queue.batches), now, rate, now - start < self.adapter.initial_stage_us)
-                    for b in [b for b in queue.batches if plan.is_skip(b.id)]:
+                    for b in [b for b in queue.batches if b.id in plan.assignments and plan.is_skip(b.id)]:
                         queue.remove(b)
                         finalize(b, None, None, r, 0, now)
                     if not queue.batches:

@@ -331,3 +331,16 @@ def test_realtime_engine_runs_replicas_concurrently():
         assert all(b1 <= a2 + 5000 for (a1, b1), (a2, b2) in zip(iv, iv[1:]))  # one batch at a time (host jitter slack)
     overlap = any(a1 < b2 and a2 < b1 for (a1, b1, r1) in runs for (a2, b2, r2) in runs if r1 != r2)
     assert overlap
+
+
+def test_engine_dp_horizon_plans_only_the_queue_head():
+    """EngineConfig.dp_horizon (real-time planning budget): batches beyond the horizon are left
+    unplanned (not skipped) and dispatched by later plans; outcomes stay complete."""
+    g = GammaList((-8, 0, 8))
+    table = _table(g.values, tasks=tuple(t.task for t in PAPER_QUERY_TYPES), base_us=300)
+    cfg = AdapterConfig(gammas=g, rate_map=PAPER_RATE_MAP.__class__(((0, 0),)), initial_stage_us=0)
+    qs = gen_poisson([(0, 6000)], 0.5, seed=9)
+    rep = ServingEngine(TableExecutor(table), table, adapter=cfg,
+                        cfg=EngineConfig(policy="otas", seed=3, dp_horizon=4, frontier_cap=8)).run(qs)
+    assert sum(rep.outcome_counts.values()) == len(qs)
+    assert rep.executed_batches > 0

@@ -42,6 +42,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--policies", default="otas,-20,0,8")
     ap.add_argument("--out", default="gpurun_out/serve_trace")
+    ap.add_argument("--dp-horizon", type=int, default=16, help="Alg. 2 over the earliest-deadline K batches per plan")
+    ap.add_argument("--frontier-cap", type=int, default=16, help="DP frontier states per row")
     ap.add_argument("--clock", default="realtime", choices=["realtime", "virtual"],
                     help="realtime: replicas execute concurrently against the wall clock (AsyncGpuExecutor); "
                          "virtual: deterministic discrete-event clock, batches executed one at a time")
@@ -67,7 +69,8 @@ def main():
         policy = pol if pol == "otas" else int(pol)
         qs = gen_poisson(profile, args.duration, seed=args.seed)
         w0 = time.time()
-        eng = ServingEngine(executor, table, adapter=adapter, cfg=EngineConfig(policy=policy, seed=args.seed))
+        ecfg = EngineConfig(policy=policy, seed=args.seed, dp_horizon=args.dp_horizon, frontier_cap=args.frontier_cap)
+        eng = ServingEngine(executor, table, adapter=adapter, cfg=ecfg)
         rep = eng.run_realtime(qs) if args.clock == "realtime" else eng.run(qs)
         wall = time.time() - w0
         rep.export(os.path.join(args.out, f"policy_{pol}"))
@@ -79,7 +82,8 @@ def main():
                 "executed_images": s["executed_images"],
                 "served_images_per_s_virtual": round(s["executed_images"] / max(s["end_s"], 1e-9), 1),
                 "gpu_busy_frac": [round(b / max(s["end_s"], 1e-9), 3) for b in s["busy_s"]],
-                "host_wall_s": round(wall, 2), "clock": args.clock}
+                "host_wall_s": round(wall, 2), "clock": args.clock, "dp_horizon": args.dp_horizon,
+                "frontier_cap": args.frontier_cap}
         results[pol] = line
         print(json.dumps(line), flush=True)
     print(json.dumps({"rate_map": f.breakpoints, "profile_s": round(time.time() - t0, 1)}), flush=True)
