@@ -138,11 +138,14 @@ int head(const float* x, int B, int t_total, int D, const float* nw, const float
 // qkv activation [B, t, 3*H*c] in `qkv_dtype`, averaged over heads (ToMe k.mean(1)).
 // scratch (nullable): match_tc_scratch_bytes(B, c) bytes; with it the tcgen05 path runs
 // (TA_MATCH_BACKEND=simt forces the SIMT kernel), without it the SIMT kernel.
+// row_map (nullable): also emit the fused merge's per-row destination map (merge_map's output).
 int match(const float* metric, const void* qkv, int qkv_dtype, int B, int t, int heads, int c,
-          int r, int32_t* src, int32_t* dst, int32_t* unm, float* scratch, cudaStream_t s);
+          int r, int32_t* src, int32_t* dst, int32_t* unm, float* scratch, cudaStream_t s,
+          int32_t* row_map = nullptr);
 size_t match_tc_scratch_bytes(int B, int c);
 int match_tc(const float* metric, const void* qkv, int qkv_dtype, int B, int t, int heads, int c,
-             int r, int32_t* src, int32_t* dst, int32_t* unm, float* scratch, cudaStream_t s);
+             int r, int32_t* src, int32_t* dst, int32_t* unm, float* scratch, cudaStream_t s,
+             int32_t* row_map = nullptr);
 // Fused merge (bf16 path): merge_map turns a layer's (src, unm) into the per-row destination map
 // of EPI_BIAS_RESID_MERGE; merge_fixup, after that GEMM, computes the size-weighted rows of the
 // destination tokens that received sources (and their bf16 copy / row statistics) and the new

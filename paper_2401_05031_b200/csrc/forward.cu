@@ -39,17 +39,16 @@ int device_sm_count() {
   return count;
 }
 
-// Fused proj + merge on the bf16 LN-folded path (TA_MERGE_FUSION=1; off by default): the proj
+// Fused proj + merge on the bf16 LN-folded path (default; TA_MERGE_FUSION=0 restores the
+// separate merge kernel): the match runs before attention and also emits the row map, the proj
 // GEMM writes rows to their merged positions plus their bf16 copy / statistics, merge_fixup
-// finishes the destination rows.  Measured a wash against proj + merge_kernel (ViT-B/16 b=256
-// gamma=-16, ncu launch lists: 5473 vs 5466 us per forward; the epilogue's bf16-copy / statistics
-// writes cost the proj GEMM as much as the merge kernel they replace), so the separate merge
-// kernel stays the default.
+// finishes the destination rows.  One full read + write of the fp32 residual less per merge
+// layer than proj + merge_kernel.
 int merge_fusion_enabled() {
   static int on = -1;
   if (on < 0) {
     const char* v = getenv("TA_MERGE_FUSION");
-    on = (v && v[0] == '1') ? 1 : 0;
+    on = (v && v[0] == '0') ? 0 : 1;
   }
   return on;
 }
@@ -544,7 +543,9 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
     // positions itself (EPI_BIAS_RESID_MERGE); otherwise the classic order proj -> match -> merge.
     int32_t *src = w.src, *dst = w.dst, *unm = w.unm;
     const bool fuse_merge = r > 0 && fused && merge_fusion_enabled() && gemm_pair_path(M, D);
-    auto do_match = [&]() -> int {
+    // row_map (fused merge): the match kernel emits the destination map itself; a forced trace
+    // gets it from merge_map.
+    auto do_match = [&](int32_t* row_map) -> int {
       const int na = (t + 1) / 2;
       const int32_t* base = forced_trace ? forced_trace : merge_trace;
       if (base) {
@@ -554,16 +555,16 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
       }
       trace_off += static_cast<size_t>(B) * (2 * r + na - r);
       if (!forced_trace)
-        return match(nullptr, w.qkv, act, B, t, d.heads, m->hd, r, src, dst, unm, w.match_scratch, st);
+        return match(nullptr, w.qkv, act, B, t, d.heads, m->hd, r, src, dst, unm, w.match_scratch, st,
+                     row_map);
       if (merge_trace)
         cudaMemcpyAsync(merge_trace + (src - forced_trace), src,
                         sizeof(int32_t) * static_cast<size_t>(B) * (2 * r + na - r),
                         cudaMemcpyDeviceToDevice, st);
-      return TA_OK;
+      return row_map != nullptr ? merge_map(src, unm, B, t, r, row_map, st) : TA_OK;
     };
     if (fuse_merge) {
-      TA_TRY(do_match());
-      TA_TRY(merge_map(src, unm, B, t, r, w.row_map, st));
+      TA_TRY(do_match(w.row_map));
       prof.mark(TA_STAGE_MATCH, l);
     }
     TA_TRY(attention(w.qkv, size, B, t, d.heads, m->hd, w.attn, act, st));
@@ -599,7 +600,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         TA_TRY(merge_fixup(w.x[cur ^ 1], w.side, size, w.size[size_buf], B, t, D, r, src, dst, unm, w.h,
                            ln2_stats, st));
       } else {
-        TA_TRY(do_match());
+        TA_TRY(do_match(nullptr));
         prof.mark(TA_STAGE_MATCH, l);
         TA_TRY(merge(w.x[cur], size, B, t, D, r, src, dst, unm, static_cast<const float*>(Lw.ln2_w),
                      static_cast<const float*>(Lw.ln2_b), w.x[cur ^ 1], w.size[size_buf], w.h, act,

@@ -62,7 +62,8 @@ template <typename QT, int kU, int kTerms, int kThreads>  // kU: 64-column passe
 __global__ void __launch_bounds__(kThreads, kThreads == 256 ? 2 : 1)
     match_fused_kernel(const float* __restrict__ metric, const QT* __restrict__ qkv, int t,
                        int heads, int c, int cp, int r, int32_t* __restrict__ src_out,
-                       int32_t* __restrict__ dst_out, int32_t* __restrict__ unm_out) {
+                       int32_t* __restrict__ dst_out, int32_t* __restrict__ unm_out,
+                       int32_t* __restrict__ row_map) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -312,8 +313,14 @@ __global__ void __launch_bounds__(kThreads, kThreads == 256 ? 2 : 1)
       int pos = 0;
       for (int j = 0; j < i; ++j) pos += rank[j] >= r;
       unm_out[static_cast<long long>(b) * (na - r) + pos] = i;
+      if (row_map != nullptr) row_map[static_cast<long long>(b) * t + 2 * i] = b * (t - r) + pos;
     }
+    // fused merge (merge_map semantics, tome.cu): merged-away A token -> side row b r + rank
+    if (row_map != nullptr && rk < r) row_map[static_cast<long long>(b) * t + 2 * i] = -1 - (b * r + rk);
   }
+  if (row_map != nullptr)  // B token j -> after the unmerged A tokens
+    for (int j = tid; j < nb; j += kThreads)
+      row_map[static_cast<long long>(b) * t + 2 * j + 1] = b * (t - r) + (na - r) + j;
   __syncthreads();
   MTRACE(4);
   if (warp == 0) {
@@ -346,7 +353,8 @@ size_t match_tc_scratch_bytes(int, int) { return 256; }
 
 // Returns TA_ERR_SHAPE outside the kernel's envelope (t > 257, c > 96 or > 16 heads).
 int match_tc(const float* metric, const void* qkv, int qkv_dtype, int B, int t, int heads, int c,
-             int r, int32_t* src, int32_t* dst, int32_t* unm, float* scratch, cudaStream_t s) {
+             int r, int32_t* src, int32_t* dst, int32_t* unm, float* scratch, cudaStream_t s,
+             int32_t* row_map) {
   (void)scratch;
   const int na = (t + 1) / 2;
   if (r <= 0 || r > na - 1 || t < 3) return TA_ERR_INVALID;
@@ -371,13 +379,13 @@ int match_tc(const float* metric, const void* qkv, int qkv_dtype, int B, int t, 
   }
   if (metric != nullptr || qkv_dtype == TA_DTYPE_F32)
     e = launch_pdl(match_fused_kernel<float, 2, 3, kFusedThreads>, dim3(B), dim3(kFusedThreads), smem3, s,
-                   metric, static_cast<const float*>(qkv), t, heads, c, cp, r, src, dst, unm);
+                   metric, static_cast<const float*>(qkv), t, heads, c, cp, r, src, dst, unm, row_map);
   else if (c <= 64)
     e = launch_pdl(match_fused_kernel<__nv_bfloat16, 1, 1, 256>, dim3(B), dim3(256), smem1, s, metric,
-                   static_cast<const __nv_bfloat16*>(qkv), t, heads, c, cp, r, src, dst, unm);
+                   static_cast<const __nv_bfloat16*>(qkv), t, heads, c, cp, r, src, dst, unm, row_map);
   else
     e = launch_pdl(match_fused_kernel<__nv_bfloat16, 2, 1, 256>, dim3(B), dim3(256), smem1, s, metric,
-                   static_cast<const __nv_bfloat16*>(qkv), t, heads, c, cp, r, src, dst, unm);
+                   static_cast<const __nv_bfloat16*>(qkv), t, heads, c, cp, r, src, dst, unm, row_map);
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 

@@ -135,11 +135,12 @@ static int match_backend() {
 }
 
 int match(const float* metric, const void* qkv, int qkv_dtype, int B, int t, int heads, int c,
-          int r, int32_t* src, int32_t* dst, int32_t* unm, float* scratch, cudaStream_t s) {
+          int r, int32_t* src, int32_t* dst, int32_t* unm, float* scratch, cudaStream_t s,
+          int32_t* row_map) {
   const int na = (t + 1) / 2, nb = t / 2;
   if (r <= 0 || r > na - 1 || t < 3) return TA_ERR_INVALID;
   if (scratch != nullptr && match_backend() == 0) {
-    const int rc = match_tc(metric, qkv, qkv_dtype, B, t, heads, c, r, src, dst, unm, scratch, s);
+    const int rc = match_tc(metric, qkv, qkv_dtype, B, t, heads, c, r, src, dst, unm, scratch, s, row_map);
     if (rc != TA_ERR_SHAPE) return rc;
   }
   const size_t smem = (static_cast<size_t>(na + nb) * (c + 1) + 3 * na) * sizeof(float);
@@ -166,7 +167,8 @@ int match(const float* metric, const void* qkv, int qkv_dtype, int B, int t, int
     e = cudaLaunchKernelEx(&cfg, k, metric, static_cast<const __nv_bfloat16*>(qkv), t, heads, c,
                            r, src, dst, unm);
   }
-  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+  if (e != cudaSuccess) return set_last_cuda_error(e);
+  return row_map != nullptr ? merge_map(src, unm, B, t, r, row_map, s) : TA_OK;
 }
 
 // ------------------------------------------------------------------ merge + LN2

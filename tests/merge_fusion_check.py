@@ -23,7 +23,10 @@ for gamma in (-16, -8):
     ref_path = os.path.join(sys.argv[1], f"fusion0_g{gamma}.pt")  # the default path's trace, if run
     shared = torch.load(ref_path)["trace"].cuda() if os.path.exists(ref_path) else trace.clone()
     forced = bb.forward_raw(imgs, ids, gamma, forced_trace=shared)
+    # own trace replayed: with fusion the free-running row map comes from the match kernel and
+    # the forced one from merge_map, so equal logits pin the two maps to each other
+    replay = bb.forward_raw(imgs, ids, gamma, forced_trace=trace.clone())
     torch.cuda.synchronize()
-    torch.save({"out": out.cpu(), "forced": forced.cpu(), "trace": trace.cpu()},
+    torch.save({"out": out.cpu(), "forced": forced.cpu(), "trace": trace.cpu(), "replay": replay.cpu()},
                os.path.join(sys.argv[1], f"fusion{os.environ.get('TA_MERGE_FUSION', '0')}_g{gamma}.pt"))
 print("ok")

@@ -188,8 +188,10 @@ def test_ln_fold_outlier_channels(gamma):
 
 
 def test_merge_fusion_matches_merge_kernel(tmp_path):
-    """The optional fused proj + merge path (TA_MERGE_FUSION=1) gives the same merge decisions
-    and, with the same forced trace, logits within the bf16 bound of the default path."""
+    """The fused proj + merge path (TA_MERGE_FUSION=1, the bf16 default) and the separate merge
+    kernel (TA_MERGE_FUSION=0) give, with the same forced trace, logits within the bf16 bound of
+    each other; each path replays its own free-running trace bit for bit (fused: the match
+    kernel's row map = merge_map's)."""
     import os
     import subprocess
     import sys
@@ -209,3 +211,5 @@ def test_merge_fusion_matches_merge_kernel(tmp_path):
         # free-running traces may differ (bf16 near-ties, as between any two bf16 kernels: SURVEY
         # App. C); both are complete and well-formed
         assert a["trace"].shape == b["trace"].shape and (b["trace"] >= 0).all()
+        for run in (a, b):
+            assert torch.equal(run["out"], run["replay"])

@@ -25,6 +25,19 @@ __global__ void rate(float* out, unsigned long long* clk, int iters) {
         uint32_t p; asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(v[i]), "f"(v[(i + 1) & 7]));
         v[i] = __uint_as_float(p) * 1.0001f;
       }
+      if (kMode == 5) {  // ex2.approx.f16x2: two exponentials per lane and instruction
+        uint32_t h = __float_as_uint(v[i]), y;
+        asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(h));
+        v[i] = __uint_as_float(y ^ 0x80008000u);
+      }
+      if (kMode == 6) {  // the softmax chunk in f16: x = s c - m (FFMA2), cvt f16x2, ex2 f16x2, hmul2 weight
+        const uint64_t x = ffma2(w[i], a, b);
+        uint32_t h, y, z;
+        asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(__uint_as_float((uint32_t)(x >> 32))), "f"(__uint_as_float((uint32_t)x)));
+        asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(h));
+        asm volatile("mul.rn.f16x2 %0, %1, %2;" : "=r"(z) : "r"(y), "r"(0x3c003c00u));
+        w[i] = x ^ z;
+      }
       if (kMode == 4) {  // ex2 + one pack per element pair
         v[i] = ex2(v[i]) * -0.5f;
         uint32_t p; asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(v[i]), "f"(v[(i + 1) & 7]));
@@ -60,5 +73,7 @@ int main() {
   for (int w : {8, 16}) run<2>("mix ex2 + 2 ffma2", w, d, c);
   for (int w : {8, 16}) run<3>("bf16x2 pack (+fmul)", w, d, c);
   for (int w : {8, 16}) run<4>("ex2 + bf16x2 pack", w, d, c);
+  for (int w : {4, 8, 16}) run<5>("ex2.f16x2 (instr)", w, d, c);
+  for (int w : {8, 16}) run<6>("f16 chunk (pairs)", w, d, c);
   return 0;
 }
