@@ -72,6 +72,7 @@ struct AttnTcLayout {
   int n_s;      // TMEM S slots (2 when t_pad <= 256)
   int rowsplit; // 1: softmax group g owns every other tile (t_pad <= 128); 0: groups split keys
   int o_col;    // single S slot with O in its own TMEM columns [o_col, o_col + hd) (0: O aliases S)
+  int qswap;    // row split, two query tiles: odd items take their tiles in reverse order
   uint32_t kv_bytes;  // per slot: K then V
   uint32_t kv_off, p_off, bias_off, red_off, bar_off, smem_bytes;
 };
@@ -98,6 +99,9 @@ AttnTcLayout attn_layout(int t, int hd) {
   L.rowsplit = L.t_pad <= 256;
   if (const char* e = getenv("TA_ATTN_SPLIT"))  // profiling override: "row" / "key"
     L.rowsplit = L.t_pad <= 256 && e[0] != 'k';
+  L.qswap = L.rowsplit && L.n_qt == 2;
+  if (const char* e = getenv("TA_ATTN_QSWAP"))  // profiling override: "0" keeps the tile order
+    if (e[0] == '0') L.qswap = 0;
   // One S slot (t_pad > 256): when S and O fit side by side, O gets its own columns, the slot
   // is released as soon as pass 2 has read it, and S of the next tile overlaps the PV tail and
   // the (deferred) epilogue, as in two-slot mode.
@@ -143,6 +147,14 @@ __device__ unsigned int g_trace_tag[16384];
 #define TRACE(ev) do {} while (0)
 #define TRACE_DECL do {} while (0)
 #endif
+
+// Row split with two query tiles per item (128 < t <= 256): group g always owns the item's g-th
+// tile in processing order, and the second tile holds only t - 128 rows, so the two groups are
+// balanced by processing every odd item's tiles in reverse order (t = 133: the second tile has 5
+// rows, and group 1 would otherwise idle while group 0 softmaxes every full tile).
+__device__ __forceinline__ int q_order(int qt, uint32_t item_local, const AttnTcLayout& L) {
+  return (L.qswap && (item_local & 1u)) ? 1 - qt : qt;
+}
 
 // kOne: one K/V slot (L.n_kv == 1), where K and V have separate barriers and lifetimes and a
 // single S slot may keep O in its own TMEM columns (L.o_col); a template parameter so that the
@@ -270,12 +282,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (qcnt > 0) { mbar_arrive(&q_full[0]); continue; }
 #endif
           mbar_arrive_expect_tx(&q_full[0], L.q_bytes);
-          tma_load_2d(&tm, &q_full[0], sQ, h * kHD, row_base + qt * kQTile);
-          tma_load_2d(&tm, &q_full[0], sQ + kBlkBytes, h * kHD, row_base + qt * kQTile + 64);
+          const int qe = q_order(qt, it, L);  // this tile's query rows
+          tma_load_2d(&tm, &q_full[0], sQ, h * kHD, row_base + qe * kQTile);
+          tma_load_2d(&tm, &q_full[0], sQ + kBlkBytes, h * kHD, row_base + qe * kQTile + 64);
           if constexpr (kTail > 0) {
-            tma_load_2d(&tmt, &q_full[0], sQ + kQBytes, h * kHD + kHd, row_base + qt * kQTile);
+            tma_load_2d(&tmt, &q_full[0], sQ + kQBytes, h * kHD + kHd, row_base + qe * kQTile);
             tma_load_2d(&tmt, &q_full[0], sQ + kQBytes + 64 * kTail * 2, h * kHD + kHd,
-                        row_base + qt * kQTile + 64);
+                        row_base + qe * kQTile + 64);
           }
           TRACE(2);
           if (qt == 0 && split_v) {
@@ -579,13 +592,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t s_bias_g = s_bias + g * 256 * 4;
       const uint32_t la = lane_base + g * 256;
       uint32_t k = 0;  // tiles processed by this group
-      uint32_t tile = 0;
+      uint32_t tile = 0, it = 0;
       int b = b_first, h = h_first;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, next_bh(b, h)) {
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, next_bh(b, h), ++it) {
         const int row_base = b * t;
         bool have_bias = false;
-        for (int qt = 0; qt < L.n_qt; ++qt, ++tile) {
+        for (int qn = 0; qn < L.n_qt; ++qn, ++tile) {
           if (static_cast<int>(tile & 1) != g) continue;
+          const int qt = q_order(qn, it, L);
           if (!have_bias) {
             named_bar_sync(2 + g, 128);  // group done with the previous item's bias
             for (int j = i; j < L.t_pad; j += 128)

@@ -63,10 +63,11 @@ struct GemmEpi {
   const float* c1 = nullptr;        // consumer: [N]
   const float* c2 = nullptr;        // consumer: [N]
   float inv_dim = 0.f;              // consumer: 1 / D
-  // EPI_BIAS_RESID_MERGE: output row of input row m (>= 0: row of out / xh / stats; < 0: row
-  // -1 - value of side), from merge_map
+  // EPI_BIAS_RESID_MERGE: output row of input row m in `out`, from the match kernel / merge_map:
+  // rows [0, rows_out) are the layer's merged rows (they also get the bf16 copy and statistics),
+  // rows [rows_out, M) the merged-away source tokens (image b's k-th source at rows_out + b r + k),
+  // which merge_fixup folds into their destinations.
   const int32_t* row_map = nullptr;
-  float* side = nullptr;
   int skip = 0;                     // profiling only (TA_GEMM_SKIP_EPILOGUE=1): no epilogue work
   int direct_store = 0;             // TA_GEMM_STORE=direct: STG.256 rows instead of TMA boxes
 };

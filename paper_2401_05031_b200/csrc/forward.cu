@@ -156,8 +156,8 @@ struct Workspace {
   float* match_scratch;
   float* stats[2];  // LN-folded path: per-row (sum, sumsq) for LN1 / LN2
   void* tf32_scratch;  // fp32 mode: tf32 hi / lo operand split of the 3xTF32 GEMMs
-  int32_t* row_map;  // fused merge: destination of every input row (merge_map)
-  float* side;       // fused merge: the merged-away source rows [B, r_max, D]
+  int32_t* row_map;  // fused merge: destination of every input row (merge_map); the merged-away
+                     // source rows land after the merged rows in x (rows <= B t_max)
   size_t total;
 };
 
@@ -195,7 +195,6 @@ Workspace carve(const ta_model* m, int B, const Schedule& s, char* base) {
                                                         std::max(m->d.mlp_dim, m->kp))
                             : 0);
   w.row_map = reinterpret_cast<int32_t*>(take(r_max > 0 ? rows * 4 : 0));
-  w.side = reinterpret_cast<float*>(take(static_cast<size_t>(B) * r_max * D * 4));
   w.total = off;
   return w;
 }
@@ -580,7 +579,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         e.stats = ln2_stats;
         e.stat_slots = stat_slots;
         e.row_map = w.row_map;
-        e.side = w.side;
+        e.rows_out = B * (t - r);  // merged rows; the r source rows per image follow them
         TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID_MERGE, e, st, w.tf32_scratch));
       prof.mark(TA_STAGE_PROJ, l);
       } else if (fused && r == 0) {
@@ -597,7 +596,8 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
     int tp = t;
     if (r > 0) {
       if (fuse_merge) {
-        TA_TRY(merge_fixup(w.x[cur ^ 1], w.side, size, w.size[size_buf], B, t, D, r, src, dst, unm, w.h,
+        TA_TRY(merge_fixup(w.x[cur ^ 1], w.x[cur ^ 1] + static_cast<size_t>(B) * (t - r) * D, size,
+                           w.size[size_buf], B, t, D, r, src, dst, unm, w.h,
                            ln2_stats, st));
       } else {
         TA_TRY(do_match(nullptr));

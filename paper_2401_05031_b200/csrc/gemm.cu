@@ -694,9 +694,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           orow = bm * epi.rows_out + epi.row_off + (m - bm * epi.rows_in);
         }
         constexpr bool kMerge = EPI == EPI_BIAS_RESID_MERGE;
-        if constexpr (kMerge) orow = row_ok ? __ldg(epi.row_map + m) : 0;
+        if constexpr (kMerge) orow = row_ok ? __ldg(epi.row_map + m) : M;  // M: past the tensor
         // rows that get a bf16 copy and statistics: every valid row, except merged-away sources
-        const bool keep_row = row_ok && (!kMerge || orow >= 0);
+        const bool keep_row = row_ok && (!kMerge || orow < epi.rows_out);
         // compute(c): TMEM columns of box c -> bias / LN / GELU / residual -> 8 packed 16-byte
         // words of this thread's row (w); stage_store(c, w): swizzled staging box + TMA store.
         auto compute = [&](int c, uint4 (&w)[8]) -> bool {
@@ -838,7 +838,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           }
           fence_proxy_async_shared();
           __syncwarp();
-          if (lane == 0 && epi.skip != 2) {
+          if constexpr (kMerge) {
+            // merged positions: eight 4-row scatters of the box (rows >= M are dropped by TMA)
+            const int dst = static_cast<int>(orow);
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+              const int r0 = __shfl_sync(0xffffffffu, dst, 4 * g), r1 = __shfl_sync(0xffffffffu, dst, 4 * g + 1);
+              const int r2 = __shfl_sync(0xffffffffu, dst, 4 * g + 2), r3 = __shfl_sync(0xffffffffu, dst, 4 * g + 3);
+              if (lane == 0 && epi.skip != 2) tma_scatter4(&tmC, smem_u32(sbuf) + g * 512, n0, r0, r1, r2, r3);
+            }
+            if (lane == 0 && epi.skip != 2) bulk_commit_group();
+          } else if (lane == 0 && epi.skip != 2) {
             if constexpr (kRemap) {
               // 3D view [B][rows_out][N]: the box goes to image b at its in-image row.
               const int b = static_cast<int>(m_base / epi.rows_in);
@@ -858,10 +868,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
         auto direct_store = [&](int c, const uint4 (&w)[8]) {
           if (!row_ok || epi.skip == 2) return;
           const int n0 = n_blk * BN + col0 + c * CW;
-          OutT* row_ptr = static_cast<OutT*>(epi.out) + m * N;
-          if constexpr (kMerge)  // x' row, or the side row of a merged-away source token
-            row_ptr = orow >= 0 ? static_cast<OutT*>(epi.out) + orow * N
-                                : reinterpret_cast<OutT*>(epi.side) + (-1 - orow) * N;
+          OutT* row_ptr = static_cast<OutT*>(epi.out) + (kMerge ? orow : m) * N;
           uint4* dst = reinterpret_cast<uint4*>(row_ptr + n0);
 #pragma unroll
           for (int j = 0; j < 4; ++j) stg256(dst + 2 * j, w[2 * j], w[2 * j + 1]);
@@ -870,7 +877,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
         for (int c = 0; c < NCH; ++c) {
           uint4 w[8];
           if (compute(c, w)) {
-            if (kMerge || (!kRemap && epi.direct_store))
+            if (!kRemap && epi.direct_store)
               direct_store(c, w);
             else
               stage_store(c, w);
@@ -1083,13 +1090,13 @@ static int launch_bf16(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
 
 // Output tensor map for the TMA-store epilogue: [M, N] row-major, 32-row x 128-byte boxes, SW128.
 static int make_tmap_out(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
-                         bool bf16) {
+                         bool bf16, uint32_t box_rows = 32) {
   auto enc = get_encode_fn();
   if (!enc) return TA_ERR_CUDA;
   const uint64_t es = bf16 ? 2 : 4;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * es};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / es), 32};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / es), box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1144,9 +1151,10 @@ static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
     attr_done(attr_mask);
   }
   CUtensorMap tc_{};
-  if (Cfg::kTma && EPI != EPI_BIAS_RESID_MERGE) {  // the merge kind stores rows directly
+  if (Cfg::kTma) {  // the merge kind: one-row boxes for tile::scatter4 over the M rows of out
     const int rc = kRemap ? make_tmap_out3(&tc_, epi.out, M / epi.rows_in, epi.rows_out, N, sizeof(OutT) == 2)
-                          : make_tmap_out(&tc_, epi.out, M, N, sizeof(OutT) == 2);
+                          : make_tmap_out(&tc_, epi.out, M, N, sizeof(OutT) == 2,
+                                          EPI == EPI_BIAS_RESID_MERGE ? 1 : 32);
     if (rc) return rc;
   }
   const int tiles = ((M + 255) / 256) * (N / 256);

@@ -315,8 +315,10 @@ __global__ void __launch_bounds__(kThreads, kThreads == 256 ? 2 : 1)
       unm_out[static_cast<long long>(b) * (na - r) + pos] = i;
       if (row_map != nullptr) row_map[static_cast<long long>(b) * t + 2 * i] = b * (t - r) + pos;
     }
-    // fused merge (merge_map semantics, tome.cu): merged-away A token -> side row b r + rank
-    if (row_map != nullptr && rk < r) row_map[static_cast<long long>(b) * t + 2 * i] = -1 - (b * r + rk);
+    // fused merge (merge_map semantics, tome.cu): merged-away A token -> source row
+    // B (t - r) + b r + rank, after the layer's merged rows
+    if (row_map != nullptr && rk < r)
+      row_map[static_cast<long long>(b) * t + 2 * i] = static_cast<int>(gridDim.x) * (t - r) + b * r + rk;
   }
   if (row_map != nullptr)  // B token j -> after the unmerged A tokens
     for (int j = tid; j < nb; j += kThreads)

@@ -224,6 +224,16 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
       "r"(smem_u32(src)), "r"(x), "r"(y)
       : "memory");
 }
+// Four 128-byte rows of a smem box (512 contiguous bytes, SW128 like the 2D boxes) to four
+// arbitrary rows of a 2D tensor whose map has a one-row box; rows past the tensor are dropped.
+__device__ __forceinline__ void tma_scatter4(const CUtensorMap* map, uint32_t src, int32_t x, int32_t r0,
+                                             int32_t r1, int32_t r2, int32_t r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(src), "r"(x), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int32_t x,
                                              int32_t y, int32_t z) {
   asm volatile(

@@ -345,7 +345,8 @@ static int merge_dispatch(const float* x, const float* size, int B, int t, int D
 // ------------------------------------------------------------------ fused merge (bf16 path)
 // merge_map: per input row of a layer, where the proj GEMM (EPI_BIAS_RESID_MERGE) writes it:
 // unmerged A token -> its position in x' (ToMe output order [A_unm ; B]), B token -> its
-// position after the unmerged A tokens, merged-away A token (src rank k) -> side row b r + k.
+// position after the unmerged A tokens, merged-away A token (src rank k) -> row B tp + b r + k
+// (the source rows follow the B tp merged rows in the same buffer).
 __global__ void __launch_bounds__(256) merge_map_kernel(const int32_t* __restrict__ src,
                                                         const int32_t* __restrict__ unm, int t, int r,
                                                         int32_t* __restrict__ row_map) {
@@ -358,12 +359,12 @@ __global__ void __launch_bounds__(256) merge_map_kernel(const int32_t* __restric
   for (int p = threadIdx.x; p < n_unm; p += blockDim.x)
     row_map[in0 + 2 * unm[static_cast<long long>(b) * n_unm + p]] = out0 + p;
   for (int k = threadIdx.x; k < r; k += blockDim.x)
-    row_map[in0 + 2 * src[static_cast<long long>(b) * r + k]] = -1 - (b * r + k);
+    row_map[in0 + 2 * src[static_cast<long long>(b) * r + k]] = static_cast<int>(gridDim.x) * tp + b * r + k;
   for (int j = threadIdx.x; j < nb; j += blockDim.x) row_map[in0 + 2 * j + 1] = out0 + n_unm + j;
 }
 
 // merge_fixup: x' already holds every kept token's row (written by the proj GEMM) and `side`
-// the merged-away sources.  Each destination B token that received sources becomes
+// (= x' + B tp rows) the merged-away sources.  Each destination B token that received sources becomes
 // (s_d x_d + sum_k s_k x_k) / (s_d + sum_k s_k) in merge_kernel's order (self, then sources by
 // rank), with its bf16 copy and whole-row statistics (slot 0); block y == 0 also writes the new
 // size vector (ToMe merge_wavg's size sum).  One warp per destination (at its first source).
