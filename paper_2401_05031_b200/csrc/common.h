@@ -70,6 +70,7 @@ struct GemmEpi {
   const int32_t* row_map = nullptr;
   int skip = 0;                     // profiling only (TA_GEMM_SKIP_EPILOGUE=1): no epilogue work
   int direct_store = 0;             // TA_GEMM_STORE=direct: STG.256 rows instead of TMA boxes
+  int resid_ldg = 0;                // TA_GEMM_RESID=ldg: residual rows by per-thread loads
 };
 
 __host__ __device__ inline long long epi_out_row(const GemmEpi& e, long long m) {

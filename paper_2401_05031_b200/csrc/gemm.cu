@@ -516,21 +516,25 @@ struct PairCfg {
   static constexpr bool kTma = pair_tma(EPI, kRemap);
   // (16 epilogue warps with one box each measured slower than 8 with two: register spills)
   static constexpr int kWarps = pair_epi_warps(EPI, kRemap);
-  static constexpr int kBufs = TA_GEMM_BUFS;  // staging boxes per epilogue warp
+  // Residual kinds read the residual through the same staging boxes: TMA loads box c + 1 into
+  // the warp's other box while box c is finished (TA_GEMM_RESID=ldg: per-thread row loads).
+  static constexpr bool kResidTma = kTma && epi_is_resid(EPI) && sizeof(OutT) == 4;
+  static constexpr int kBufs = kResidTma ? 2 : TA_GEMM_BUFS;  // staging boxes per epilogue warp
   static constexpr int kThreads = 128 + 32 * kWarps;
   static constexpr int kABytes = 128 * kBK * 2;
   static constexpr int kBBytes = 128 * kBK * 2;  // this CTA's half of the 256-row W tile
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kEpiBytes = kTma ? kWarps * kBufs * 4096 : kEpiWarps * 32 * 32 * 4;
   static constexpr int kStages = kEpiBytes > 32768 ? 5 : 6;
-  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 256;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 512;
 };
 
 template <int EPI, typename OutT, bool kRemap>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, kRemap>::kThreads, 1)
     gemm_bf16_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                                 const __grid_constant__ CUtensorMap tmB,
-                                const __grid_constant__ CUtensorMap tmC, int M, int N, int K,
+                                const __grid_constant__ CUtensorMap tmC,
+                                const __grid_constant__ CUtensorMap tmR, int M, int N, int K,
                                 GemmEpi epi) {
   using Cfg = PairCfg<EPI, OutT, kRemap>;
   constexpr int BN = 256;
@@ -544,7 +548,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rfull = tempty + 2;  // [kWarps][kBufs]: residual box landed (kResidTma)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + Cfg::kWarps * Cfg::kBufs);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -555,6 +560,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     if constexpr (Cfg::kTma) tma_prefetch(&tmC);
+    if constexpr (Cfg::kResidTma) tma_prefetch(&tmR);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < S; ++s) {
@@ -565,6 +571,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * Cfg::kWarps);  // one arrive per epilogue warp of both CTAs
     }
+    if constexpr (Cfg::kResidTma)
+      for (int i = 0; i < Cfg::kWarps * Cfg::kBufs; ++i) mbar_init(&rfull[i], 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc_pair<512>(tmem_slot);
@@ -652,10 +660,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
     int acc = 0;
     uint32_t acc_phase = 0;
     int tma_buf = 0;
+    uint32_t r_par = 0u;  // kResidTma: bit b = mbarrier parity of staging box b's next load
+    const bool resid_tma = Cfg::kResidTma && !epi.resid_ldg;
     for (int tile = cid; tile < num_tiles; tile += ncl) {
       const int m_blk = tile / num_n;
       const int n_blk = tile - m_blk * num_n;
       const long long m_base = static_cast<long long>(m_blk) * 256 + rank * 128 + q * 32;
+      // kResidTma: the residual box c (32 rows x 32 fp32 of this warp's columns) goes by TMA
+      // into staging box c & 1, once that box's previous store has read it; box 0 before the
+      // accumulator wait, box c + 1 while box c is finished.
+      auto resid_load = [&](int c) {
+        if constexpr (Cfg::kResidTma) {
+          if (lane == 0) {
+            const int b = c & 1;
+            bulk_wait_group_read<0>();
+            uint64_t* bar = &rfull[ew * Cfg::kBufs + b];
+            mbar_arrive_expect_tx(bar, 4096);
+            tma_load_2d(&tmR, bar, epi_smem + (ew * Cfg::kBufs + b) * 4096,
+                        n_blk * BN + col0 + c * 32, static_cast<int>(m_base));
+          }
+          __syncwarp();
+        }
+      };
+      if (resid_tma && !epi.skip) resid_load(0);
       if constexpr (epi_is_resid(EPI)) {
         // Pull this warp's residual rows into L2 while the MMAs run.
         const long long m = m_base + lane;
@@ -717,8 +744,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
             if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
           }
           if (epi.skip == 1) return false;
+          if constexpr (Cfg::kResidTma) {
+            if (resid_tma) {
+              if (c + 1 < NCH) resid_load(c + 1);
+              const int b = c & 1;
+              mbar_wait(&rfull[ew * Cfg::kBufs + b], (r_par >> b) & 1u);
+              r_par ^= 1u << b;
+              // this row's 32 residual values: SW128 chunk j at (j ^ (row & 7))
+              const uint32_t srow = smem_u32(epi_smem + (ew * Cfg::kBufs + b) * 4096) + lane * 128;
+#pragma unroll
+              for (int j = 0; j < CW / 4; ++j) {
+                const float4 rr = lds_f4(srow + ((j ^ (lane & 7)) << 4));
+                const float2 lo = f2_unpack(fadd2(f2_pack(v[4 * j], v[4 * j + 1]), f2_pack(rr.x, rr.y)));
+                const float2 hi = f2_unpack(fadd2(f2_pack(v[4 * j + 2], v[4 * j + 3]), f2_pack(rr.z, rr.w)));
+                v[4 * j] = lo.x;
+                v[4 * j + 1] = lo.y;
+                v[4 * j + 2] = hi.x;
+                v[4 * j + 3] = hi.y;
+              }
+            }
+          }
           if constexpr (epi_is_resid(EPI) || epi_is_patch(EPI)) {
-            if (row_ok) {
+            if (row_ok && !(Cfg::kResidTma && resid_tma)) {
               const float4* rp =
                   epi_is_resid(EPI)
                       ? reinterpret_cast<const float4*>(epi.resid + m * N + n0)
@@ -812,8 +859,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
         };
         auto stage_store = [&](int c, const uint4 (&w)[8]) {
           const int n0 = n_blk * BN + col0 + c * CW;
+          if (Cfg::kResidTma && resid_tma) tma_buf = c & 1;  // the residual's box (already free)
           uint8_t* sbuf = epi_smem + (ew * Cfg::kBufs + tma_buf) * 4096;
-          if (lane == 0) bulk_wait_group_read<Cfg::kBufs - 1>();  // last store from sbuf has read it
+          if (!(Cfg::kResidTma && resid_tma) && lane == 0)
+            bulk_wait_group_read<Cfg::kBufs - 1>();  // last store from sbuf has read it
           __syncwarp();
           const uint32_t srow = smem_u32(sbuf) + lane * 128;
           // Row remap: a row of this box that belongs to a later image is also stored directly
@@ -1150,11 +1199,15 @@ static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
     if (e != cudaSuccess) return set_last_cuda_error(e);
     attr_done(attr_mask);
   }
-  CUtensorMap tc_{};
+  CUtensorMap tc_{}, tr_{};
   if (Cfg::kTma) {  // the merge kind: one-row boxes for tile::scatter4 over the M rows of out
     const int rc = kRemap ? make_tmap_out3(&tc_, epi.out, M / epi.rows_in, epi.rows_out, N, sizeof(OutT) == 2)
                           : make_tmap_out(&tc_, epi.out, M, N, sizeof(OutT) == 2,
                                           EPI == EPI_BIAS_RESID_MERGE ? 1 : 32);
+    if (rc) return rc;
+  }
+  if (Cfg::kResidTma) {  // the residual in the input row numbering, 32-row boxes
+    const int rc = make_tmap_out(&tr_, epi.resid, M, N, false);
     if (rc) return rc;
   }
   const int tiles = ((M + 255) / 256) * (N / 256);
@@ -1169,7 +1222,7 @@ static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta_, tb_, tc_, M, N, K, epi);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta_, tb_, tc_, tr_, M, N, K, epi);
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 
@@ -1251,9 +1304,14 @@ int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, b
     const char* v = getenv("TA_GEMM_STORE");
     return (v && v[0] == 'd') ? 1 : 0;
   }();
+  static const int resid_ldg = [] {  // profiling: TA_GEMM_RESID=ldg reads the residual per thread
+    const char* v = getenv("TA_GEMM_RESID");
+    return (v && v[0] == 'l') ? 1 : 0;
+  }();
   GemmEpi epi = epi_in;
   epi.skip = skip_epi;
   epi.direct_store = direct;
+  epi.resid_ldg = resid_ldg;
   if (M <= 0) return TA_OK;
   if (K % kBK != 0 || N % 128 != 0) return TA_ERR_SHAPE;
   if ((epi_is_resid(epi_kind) || epi_is_patch(epi_kind)) && out_bf16) return TA_ERR_INVALID;
