@@ -682,7 +682,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           __syncwarp();
         }
       };
-      if (resid_tma && !epi.skip) resid_load(0);
+      if (resid_tma && epi.skip != 1) resid_load(0);  // (skip 2 still finishes the boxes)
       if constexpr (epi_is_resid(EPI)) {
         // Pull this warp's residual rows into L2 while the MMAs run.
         const long long m = m_base + lane;
