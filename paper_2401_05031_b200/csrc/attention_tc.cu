@@ -268,6 +268,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                           row_base + kb * kKeyBlk);
           }
         };
+#ifdef TA_ATTN_EXP_KVONCE  // profiling only: wrong results (K / V of the first items reused)
+        if (it >= static_cast<uint32_t>(L.n_kv) && !split_v) {
+          mbar_arrive(&kv_full[kvs]);
+        } else
+#endif
+        {
         mbar_arrive_expect_tx(&kv_full[kvs], split_v ? half_bytes : 2 * half_bytes);
         for (int kb = 0; kb < L.n_kb; ++kb) {
           tma_load_2d(&tm, &kv_full[kvs], sK + kb * kBlkBytes, D + h * kHD, row_base + kb * kKeyBlk);
@@ -276,6 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         row_base + kb * kKeyBlk);
         }
         if (!split_v) load_v(&kv_full[kvs]);
+        }
         for (int qt = 0; qt < L.n_qt; ++qt, ++qcnt) {
           mbar_wait(&q_free[0], (qcnt & 1) ^ 1);
 #ifdef TA_ATTN_EXP_QONCE  // profiling only: wrong results (Q of the first tile reused)

@@ -16,16 +16,17 @@ cap() {  # name gamma regex skip
     python tools/launch_list.py $2 > /dev/null 2>&1
 }
 # demangled names read "gemm_bf16_sm100_pair_kernel<(int)7, ...>"; pair-kernel launch order at
-# gamma 0: patch (kind 5), then per layer qkv (6), proj (4), fc1 (7), fc2 (4)
+# gamma 0: patch (kind 5), then per layer qkv (6), proj (4), fc1 (7), fc2 (4); at gamma < 0 the
+# proj of a merge layer is the fused proj + merge (kind 8) followed by merge_fixup
 cap fc1_inforward 0 'pair_kernel<\(int\)7' 2      # fc1 + LN-fold + GELU, layer 2, t=197
 cap qkv_inforward 0 'pair_kernel<\(int\)6' 2      # QKV + LN-fold
 cap fc2_inforward 0 'pair_kernel<\(int\)4' 5      # fc2 + residual + stats (odd kind-4 launches at gamma 0)
 cap proj_inforward 0 'pair_kernel<\(int\)4' 4     # proj + residual + stats
-cap proj_merge_inforward -8 'pair_kernel<\(int\)2' 2  # proj + residual before a merge
+cap proj_merge_inforward -8 'pair_kernel<\(int\)8' 2  # fused proj + merge (scatter4 stores), t=181
+cap fixup_inforward -8 'merge_fixup' 2
 cap attn_t197_inforward 0 'attn_tc_kernel' 2
 cap attn_t389_inforward 16 'attn_tc_kernel' 11
 cap match_bf16_inforward -8 'match_fused_kernel' 2
-cap merge_inforward -8 'merge_kernel' 2
 cap patchify_inforward 0 'patchify' 0
 cap head_inforward 0 'head_kernel' 0
 ls -la $OUT | grep prof_${TAG}

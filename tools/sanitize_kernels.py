@@ -18,8 +18,9 @@ st = torch.cuda.current_stream().cuda_stream
 dev = "cuda"
 chk = _cuda.check
 
-# GEMMs: pair kernel (N % 256 == 0) and single-CTA kernel (small M), epilogues 0 / 1 / 2
-for M, N, K in ((300, 512, 128), (97, 256, 192), (1000, 768, 256)):
+# GEMMs: single-CTA kernel (M <= 3072 and N <= 1024) and the CTA-pair kernel (M = 4000 and
+# N = 2048; the residual kind reads its residual boxes by TMA), epilogues 0 / 1 / 2
+for M, N, K in ((300, 512, 128), (97, 256, 192), (1000, 768, 256), (4000, 768, 256), (3300, 2048, 128)):
     a = torch.randn(M, K, device=dev).bfloat16()
     w = (torch.randn(N, K, device=dev) * 0.05).bfloat16()
     bias = torch.randn(N, device=dev)
@@ -70,5 +71,15 @@ for dtype in ("bf16", "fp32"):
         sm.forward(imgs, [0, 1, 0], gamma=g)
     torch.cuda.synchronize()
     sm.backbone.close()
+# ViT-B/16 at M = B t > 3072: the CTA-pair GEMMs in the forward, incl. the fused proj + merge
+# (tile::scatter4 stores, merge_fixup) and the row-remapped prompt epilogues
+cfg, params = helpers.backbone("vit_b16")
+tasks = helpers.task_params(cfg, (10,), [4])
+imgs = helpers.synthetic_images(17, cfg.img, seed=2).cuda()
+sm = helpers.serve_model(cfg, params, tasks, dtype="bf16")
+for g in (-8, 0, 4):
+    sm.forward(imgs, [0] * 17, gamma=g)
+torch.cuda.synchronize()
+sm.backbone.close()
 torch.cuda.synchronize()
 print("sanitize_kernels: all launches done")
