@@ -31,6 +31,7 @@
 // -inf bias (their K / V rows are the next image's rows or TMA zero fill: finite, p = 0).
 #include <cfloat>
 #include <cstdlib>
+#include <type_traits>
 
 #include <cudaTypedefs.h>
 
@@ -237,7 +238,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_all = *tmem_slot;
+  const uint32_t tmem = tmem_all;
 
   grid_dep_wait();  // qkv is the previous kernel's output
 
@@ -308,12 +310,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // The whole warp runs the issuer with warp-uniform state; one elected lane issues each
+    // tcgen05.mma / commit (ptx.cuh umma_f16_w): the descriptor arithmetic stays in uniform
+    // registers, so an MMA costs a few uniform instructions instead of an R2UR + elect loop,
+    // which matters on a sub-partition shared with two softmax warps.
+    {
+      const uint32_t tmem = __shfl_sync(0xffffffffu, tmem_all, 0);  // warp-uniform TMEM base
       constexpr uint32_t idesc_pv = idesc_bf16(kQTile, kHd, /*b_mn_major=*/true);
       constexpr uint32_t idesc_pv_t = idesc_bf16(kQTile, kTail > 0 ? kTail : 16, /*b_mn_major=*/true);
       // O += P_blk V_blk for one 64-key block: N = 64 from the SW128 V part into O[0, 64) and,
       // for head_dim 80, N = 16 from the SW32 tail into O[64, 80).
-      auto pv_block = [&](uint32_t o_tmem, uint64_t pdesc, const uint8_t* sKVslot, int kb, int nkc) {
+      // kW: warp-uniform issue (the whole warp runs the caller) or lane-0 issue
+      auto mma = [](auto kW, uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+        if constexpr (decltype(kW)::value) umma_f16_w(d, a, b, id, acc);
+        else umma_f16(d, a, b, id, acc);
+      };
+      auto pv_block = [&](auto kW, uint32_t o_tmem, uint64_t pdesc, const uint8_t* sKVslot, int kb, int nkc) {
         const uint32_t vbase = smem_u32(sKVslot + L.n_kb * kBlkBytes + kb * kBlkBytes);
         const uint32_t vtbase = smem_u32(sKVslot + L.vt_off + kb * L.tail_blk);
 #pragma unroll
@@ -321,10 +333,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (kc >= nkc) break;
           // V rows (keys) are the K dimension: 16 keys = two 8-row groups = 2048 B.
           const uint64_t vdesc = umma_desc_sw128_mn(vbase + kc * 2048, 8192, 1024);
-          umma_f16(o_tmem, pdesc + 2 * kc, vdesc, idesc_pv, (kb | kc) != 0);
+          mma(kW, o_tmem, pdesc + 2 * kc, vdesc, idesc_pv, (kb | kc) != 0);
           if constexpr (kTail > 0) {
             const uint64_t vtdesc = umma_desc_sw32_mn(vtbase + kc * 512, 512, 256);
-            umma_f16(o_tmem + kHd, pdesc + 2 * kc, vtdesc, idesc_pv_t, (kb | kc) != 0);
+            mma(kW, o_tmem + kHd, pdesc + 2 * kc, vtdesc, idesc_pv_t, (kb | kc) != 0);
           }
         }
       };
@@ -348,14 +360,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
           const int nkc = kb == L.n_kb - 1 ? L.nkc_last : kKeyBlk / 16;
-          pv_block(o_tmem, pdesc, sKVslot, kb, nkc);
-          umma_commit(&p_free[ps]);
+          pv_block(std::true_type{}, o_tmem, pdesc, sKVslot, kb, nkc);
+          umma_commit_w(&p_free[ps]);
         }
-        umma_commit(&o_full[sslot]);
+        umma_commit_w(&o_full[sslot]);
         TRACE(6);
-        if (last_of_item) umma_commit(kOne ? &v_free[kvs] : &kv_free[kvs]);
+        if (last_of_item) umma_commit_w(kOne ? &v_free[kvs] : &kv_free[kvs]);
       };
       if (L.rowsplit) {
+        // lane-0 issue here: the whole-warp form polls with shuffles and measured 1-2 % slower
+        // in this loop (the blocking key-split loop below gains 4-11 % from it)
+        if (lane == 0) {
         // Row-split mode (t_pad <= 256): tile n lives in S slot n % 2 and is softmaxed by group
         // n % 2.  Non-blocking scheduler: issue whichever is ready first, the next S (at most two
         // tiles in flight) or the next PV block, so one group never waits on the other.
@@ -418,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
             const int nkc = pkb[grp] == L.n_kb - 1 ? L.nkc_last : kKeyBlk / 16;
-            pv_block(tmem + grp * 256, pdesc, sKV + kvs * L.kv_bytes, pkb[grp], nkc);
+            pv_block(std::false_type{}, tmem + grp * 256, pdesc, sKV + kvs * L.kv_bytes, pkb[grp], nkc);
             umma_commit(&p_free[ps]);
             TRACE(5 + 16 * grp);
             if (++pkb[grp] == L.n_kb) {
@@ -438,6 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               ++pdone;
             }
           }
+        }
         }
       } else {
       uint32_t it = 0, qcnt = 0, tcnt = 0;
@@ -463,15 +479,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t kdesc = umma_desc_sw128(smem_u32(sK + n0 * 128));
 #pragma unroll
             for (int k = 0; k < kHd / 16; ++k)
-              umma_f16(tmem + ss * 256 + n0, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0);
+              umma_f16_w(tmem + ss * 256 + n0, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0);
             if constexpr (kTail > 0)
-              umma_f16(tmem + ss * 256 + n0, umma_desc_sw32(smem_u32(sQ + kQBytes)),
+              umma_f16_w(tmem + ss * 256 + n0, umma_desc_sw32(smem_u32(sQ + kQBytes)),
                        umma_desc_sw32(smem_u32(sK + L.kt_off + n0 * kTail * 2)), idesc_s, 1);
           }
-          umma_commit(&s_full[ss]);
+          umma_commit_w(&s_full[ss]);
           TRACE(4);
-          umma_commit(&q_free[0]);
-          if (kOne && qt + 1 == L.n_qt) umma_commit(&kv_free[kvs]);  // the item's K is consumed
+          umma_commit_w(&q_free[0]);
+          if (kOne && qt + 1 == L.n_qt) umma_commit_w(&kv_free[kvs]);  // the item's K is consumed
           if (pend_slot >= 0) issue_pv(pend_slot, pend_kvs, pend_last, pend_first, pend_vpar);
           pend_slot = ss;
           pend_kvs = kvs;
