@@ -616,7 +616,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    // the whole warp runs the issue loop, one elected lane issues (ptx.cuh umma_f16_pair_w):
+    // descriptors stay in uniform registers instead of an R2UR + elect loop per MMA
+    if (leader) {
+      const uint32_t tmem_base_u = __shfl_sync(0xffffffffu, tmem_base, 0);
       constexpr uint32_t idesc = idesc_bf16(256, BN);
       int stage = 0;
       uint32_t phase = 0;
@@ -625,7 +628,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
       for (int tile = cid; tile < num_tiles; tile += ncl) {
         mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base_u + acc * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -635,14 +638,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           const uint64_t bdesc = umma_desc_sw128(sb);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
-            umma_f16_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
-          umma_commit_pair(&empty[stage]);
+            umma_f16_pair_w(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          umma_commit_pair_w(&empty[stage]);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit_pair(&tfull[acc]);
+        umma_commit_pair_w(&tfull[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
