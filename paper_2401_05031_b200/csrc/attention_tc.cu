@@ -55,7 +55,7 @@ constexpr int kBlkBytes = kKeyBlk * kHd * 2;  // 8 KB: one 64-row SW128 box
 constexpr int kQBytes = kQTile * kHd * 2;     // 16 KB
 constexpr int kPBytes = kQTile * kKeyBlk * 2;  // 16 KB: one P block
 constexpr int kMaxTPad = 512;
-constexpr int kThreads = 320;
+constexpr int kThreads = 352;  // 8 softmax warps, TMA warp 8, MMA warps 9 and 10
 
 struct AttnTcLayout {
   int hd;       // 64, or 80 = a 64-column SW128 part + a 16-column SW32 tail
@@ -218,10 +218,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 8 && lane == 0) {
     tma_prefetch(&tm);
     for (int s = 0; s < 2; ++s) {
+      // row split: every tile of an item releases its K / V (MMA warp 9 or 10, one per tile)
+      const int rel = L.rowsplit ? L.n_qt : 1;
       mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_free[s], 1);
+      mbar_init(&kv_free[s], rel);
       mbar_init(&v_full[s], 1);
-      mbar_init(&v_free[s], 1);
+      mbar_init(&v_free[s], rel);
       mbar_init(&q_full[s], 1);
       mbar_init(&q_free[s], 1);
       mbar_init(&s_full[s], 1);
@@ -286,17 +288,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!split_v) load_v(&kv_full[kvs]);
         }
         for (int qt = 0; qt < L.n_qt; ++qt, ++qcnt) {
-          mbar_wait(&q_free[0], (qcnt & 1) ^ 1);
+          // One Q buffer.  Row split: tile n belongs to MMA warp 9 + (n & 1), whose own barrier
+          // pair (q_full / q_free[n & 1]) completes once per tile of that warp; the buffer is
+          // reloaded once S of tile n - 1 (the other warp's) is done.  Key split: one pair.
+          uint64_t* qf = &q_full[L.rowsplit ? (qcnt & 1) : 0];
+          if (L.rowsplit) {
+            if (qcnt > 0) mbar_wait(&q_free[(qcnt - 1) & 1], ((qcnt - 1) >> 1) & 1);
+          } else {
+            mbar_wait(&q_free[0], (qcnt & 1) ^ 1);
+          }
 #ifdef TA_ATTN_EXP_QONCE  // profiling only: wrong results (Q of the first tile reused)
-          if (qcnt > 0) { mbar_arrive(&q_full[0]); continue; }
+          if (qcnt > 0) { mbar_arrive(qf); continue; }
 #endif
-          mbar_arrive_expect_tx(&q_full[0], L.q_bytes);
+          mbar_arrive_expect_tx(qf, L.q_bytes);
           const int qe = q_order(qt, it, L);  // this tile's query rows
-          tma_load_2d(&tm, &q_full[0], sQ, h * kHD, row_base + qe * kQTile);
-          tma_load_2d(&tm, &q_full[0], sQ + kBlkBytes, h * kHD, row_base + qe * kQTile + 64);
+          tma_load_2d(&tm, qf, sQ, h * kHD, row_base + qe * kQTile);
+          tma_load_2d(&tm, qf, sQ + kBlkBytes, h * kHD, row_base + qe * kQTile + 64);
           if constexpr (kTail > 0) {
-            tma_load_2d(&tmt, &q_full[0], sQ + kQBytes, h * kHD + kHd, row_base + qe * kQTile);
-            tma_load_2d(&tmt, &q_full[0], sQ + kQBytes + 64 * kTail * 2, h * kHD + kHd,
+            tma_load_2d(&tmt, qf, sQ + kQBytes, h * kHD + kHd, row_base + qe * kQTile);
+            tma_load_2d(&tmt, qf, sQ + kQBytes + 64 * kTail * 2, h * kHD + kHd,
                         row_base + qe * kQTile + 64);
           }
           TRACE(2);
@@ -308,8 +318,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 9) {
-    // ------------------------------------------------------------ MMA issuer
+  } else if (warp == 9 || warp == 10) {
+    // ------------------------------------------------------------ MMA issuer(s)
     // The whole warp runs the issuer with warp-uniform state; one elected lane issues each
     // tcgen05.mma / commit (ptx.cuh umma_f16_w): the descriptor arithmetic stays in uniform
     // registers, so an MMA costs a few uniform instructions instead of an R2UR + elect loop,
@@ -368,94 +378,62 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (last_of_item) umma_commit_w(kOne ? &v_free[kvs] : &kv_free[kvs]);
       };
       if (L.rowsplit) {
-        // lane-0 issue here: the whole-warp form polls with shuffles and measured 1-2 % slower
-        // in this loop (the blocking key-split loop below gains 4-11 % from it)
-        if (lane == 0) {
-        // Row-split mode (t_pad <= 256): tile n lives in S slot n % 2 and is softmaxed by group
-        // n % 2.  Non-blocking scheduler: issue whichever is ready first, the next S (at most two
-        // tiles in flight) or the next PV block, so one group never waits on the other.
-        const int n_my = n_items > static_cast<int>(blockIdx.x)
-                             ? (n_items - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
-                             : 0;
-        const int T = n_my * L.n_qt;
-        // Tile n uses S slot n % 2 and softmax group n % 2; each group's PV blocks are issued
-        // as soon as they are ready, independently of the other group (the O accumulators are
-        // per slot), so the two groups overlap instead of taking turns.
-        int sN = 0, pdone = 0;
-        int s_it = 0, s_qt = 0;  // (item, q tile) of tile sN
-        int pt[2] = {0, 1}, pkb[2] = {0, 0};
-        // (item, q tile) of each group's current PV tile pt[g]
-        int p_it[2] = {0, L.n_qt == 1 ? 1 : 0}, p_qt[2] = {0, L.n_qt == 1 ? 0 : 1};
-        int kv_tiles[2] = {0, 0};  // per K/V slot: tiles of the slot's item whose PV is issued
-        while (pdone < T) {
-          if (sN < T) {
-            const int slot = sN & 1;
-            const int kvs = ring_slot(s_it, L.n_kv);
-            if (mbar_test(&s_free[slot], ((sN >> 1) & 1) ^ 1) && mbar_test(&q_full[0], sN & 1) &&
-                (s_qt != 0 || mbar_test(&kv_full[kvs], ring_use(s_it, L.n_kv) & 1))) {
-              TRACE(7);
-              tc_fence_after();
-              const uint8_t* sK = sKV + kvs * L.kv_bytes;
+        // Row-split mode (t_pad <= 256): tile n (this CTA's n-th tile) lives in S slot n & 1, is
+        // softmaxed by group n & 1 and issued by MMA warp 9 + (n & 1) with blocking waits: S,
+        // then its PV blocks as its group's P stages fill, so neither group's MMAs wait behind
+        // the other group's (a single issuer polling both measured 1.3-1.6x longer per tile
+        // from the last P block to O).
+        const uint32_t g = warp - 9;
+        const uint32_t slot_tmem = tmem + g * 256;
+        uint32_t j = 0, pu = 0, n = 0, it = 0;
+        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+          const int kvs = ring_slot(it, L.n_kv);
+          const uint32_t kv_par = ring_use(it, L.n_kv) & 1;
+          const uint8_t* sKVslot = sKV + kvs * L.kv_bytes;
+          for (int qt = 0; qt < L.n_qt; ++qt, ++n) {
+            if ((n & 1u) != g) continue;
+            mbar_wait(&s_free[g], (j & 1) ^ 1);  // group g has read O of its previous tile
+            mbar_wait(&q_full[g], j & 1);
+            mbar_wait(&kv_full[kvs], kv_par);
+            TRACE(7);
+            tc_fence_after();
+            {
               const uint64_t qdesc = umma_desc_sw128(smem_u32(sQ));
               const uint32_t idesc_s = idesc_bf16(kQTile, L.t_mma);
-              const uint64_t kdesc = umma_desc_sw128(smem_u32(sK));
+              const uint64_t kdesc = umma_desc_sw128(smem_u32(sKVslot));
 #pragma unroll
               for (int k = 0; k < kHd / 16; ++k)
-                umma_f16(tmem + slot * 256, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0);
+                umma_f16_w(slot_tmem, qdesc + 2 * k, kdesc + 2 * k, idesc_s, k > 0);
               if constexpr (kTail > 0)  // head_dim 80: the 16-column tail as a fifth K step
-                umma_f16(tmem + slot * 256, umma_desc_sw32(smem_u32(sQ + kQBytes)),
-                         umma_desc_sw32(smem_u32(sK + L.kt_off)), idesc_s, 1);
-              umma_commit(&s_full[slot]);
-              umma_commit(&q_free[0]);
-              if (kOne && s_qt + 1 == L.n_qt) umma_commit(&kv_free[kvs]);  // the item's K is consumed
-              TRACE(4);
-              ++sN;
-              if (++s_qt == L.n_qt) {
-                s_qt = 0;
-                ++s_it;
-              }
+                umma_f16_w(slot_tmem, umma_desc_sw32(smem_u32(sQ + kQBytes)),
+                           umma_desc_sw32(smem_u32(sKVslot + L.kt_off)), idesc_s, 1);
             }
-          }
-#pragma unroll
-          for (int grp = 0; grp < 2; ++grp) {
-            if (pt[grp] >= sN) continue;
-            const uint32_t u = p_use[grp];
-            const int ps = 2 * grp + (u & 1);
-            if (!mbar_test(&p_full[ps], (u >> 1) & 1)) continue;
-            // head_dim 80: O[0, 80) overlaps S block 1, so block 0's PV waits for block 1's P
-            if (kTail > 0 && pkb[grp] == 0 && L.n_kb > 1 &&
-                !mbar_test(&p_full[2 * grp + ((u + 1) & 1)], ((u + 1) >> 1) & 1))
-              continue;
-            const int kvs = ring_slot(p_it[grp], L.n_kv);
-            if (kOne && pkb[grp] == 0 && !mbar_test(&v_full[kvs], p_it[grp] & 1)) continue;
-            TRACE(8 + 16 * grp);
-            ++p_use[grp];
-            tc_fence_after();
-            const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
-            const int nkc = pkb[grp] == L.n_kb - 1 ? L.nkc_last : kKeyBlk / 16;
-            pv_block(std::false_type{}, tmem + grp * 256, pdesc, sKV + kvs * L.kv_bytes, pkb[grp], nkc);
-            umma_commit(&p_free[ps]);
-            TRACE(5 + 16 * grp);
-            if (++pkb[grp] == L.n_kb) {
-              umma_commit(&o_full[grp]);
-              TRACE(6);
-              if (++kv_tiles[kvs] == L.n_qt) {  // every tile of the item has its PV issued
-                umma_commit(kOne ? &v_free[kvs] : &kv_free[kvs]);
-                kv_tiles[kvs] = 0;
-              }
-              pt[grp] += 2;
-              p_qt[grp] += 2;
-              while (p_qt[grp] >= L.n_qt) {
-                p_qt[grp] -= L.n_qt;
-                ++p_it[grp];
-              }
-              pkb[grp] = 0;
-              ++pdone;
+            umma_commit_w(&s_full[g]);
+            umma_commit_w(&q_free[g]);
+            if (kOne) umma_commit_w(&kv_free[kvs]);  // this tile's use of K is done
+            TRACE(4);
+            if (kOne) mbar_wait(&v_full[kvs], kv_par);
+            for (int kb = 0; kb < L.n_kb; ++kb) {
+              const int ps = 2 * g + (pu & 1);
+              mbar_wait(&p_full[ps], (pu >> 1) & 1);
+              ++pu;
+              // head_dim 80: O[0, 80) overlaps S block 1, so block 0's PV waits for block 1's P
+              if (kTail > 0 && kb == 0 && L.n_kb > 1) mbar_wait(&p_full[2 * g + (pu & 1)], (pu >> 1) & 1);
+              TRACE(8 + 16 * g);
+              tc_fence_after();
+              const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
+              const int nkc = kb == L.n_kb - 1 ? L.nkc_last : kKeyBlk / 16;
+              pv_block(std::true_type{}, slot_tmem, pdesc, sKVslot, kb, nkc);
+              umma_commit_w(&p_free[ps]);
+              TRACE(5 + 16 * g);
             }
+            umma_commit_w(&o_full[g]);
+            umma_commit_w(kOne ? &v_free[kvs] : &kv_free[kvs]);  // this tile's use of K / V is done
+            TRACE(6);
+            ++j;
           }
         }
-        }
-      } else {
+      } else if (warp == 9) {
       uint32_t it = 0, qcnt = 0, tcnt = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
         const int kvs = ring_slot(it, L.n_kv);
