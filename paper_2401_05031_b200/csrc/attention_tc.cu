@@ -74,6 +74,7 @@ struct AttnTcLayout {
   int rowsplit; // 1: softmax group g owns every other tile (t_pad <= 128); 0: groups split keys
   int o_col;    // single S slot with O in its own TMEM columns [o_col, o_col + hd) (0: O aliases S)
   int qswap;    // row split, two query tiles: odd items take their tiles in reverse order
+  int o_sep;    // row split: O in its own columns [256 g + o_sep, 256 g + 256) of slot g (0: aliases S)
   uint32_t kv_bytes;  // per slot: K then V
   uint32_t kv_off, p_off, bias_off, red_off, bar_off, smem_bytes;
 };
@@ -101,6 +102,15 @@ AttnTcLayout attn_layout(int t, int hd) {
   if (const char* e = getenv("TA_ATTN_SPLIT"))  // profiling override: "row" / "key"
     L.rowsplit = L.t_pad <= 256 && e[0] != 'k';
   L.qswap = L.rowsplit && L.n_qt == 2;
+  // Row split with room beside S in the slot (t_mma + hd <= 256): O gets its own columns, the
+  // slot is released as soon as pass 2 has read S, and the MMA warp computes the group's next S
+  // during this tile's PV tail and epilogue (o_free hands O back before the next tile's PV).
+  {
+    const int hd_cols = (hd + 15) / 16 * 16;
+    L.o_sep = (L.rowsplit && L.t_mma + hd_cols <= 256) ? 256 - hd_cols : 0;
+    if (const char* e = getenv("TA_ATTN_OSEP"))  // profiling override: "0" keeps O in the slot
+      if (e[0] == '0') L.o_sep = 0;
+  }
   if (const char* e = getenv("TA_ATTN_QSWAP"))  // profiling override: "0" keeps the tile order
     if (e[0] == '0') L.qswap = 0;
   // One S slot (t_pad > 256): when S and O fit side by side, O gets its own columns, the slot
@@ -195,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* p_full = bars + 14;   // [4]
   uint64_t* p_free = bars + 18;   // [4]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
+  uint64_t* o_free = bars + 27;  // [2] row split with L.o_sep: group g has read its O
 
   const uint32_t warp = warp_id(), lane = lane_id();
   // No runtime integer division in the loops below: it compiles to I2F / MUFU.RCP / F2I on
@@ -229,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&s_full[s], 1);
       mbar_init(&s_free[s], L.rowsplit ? 128 : 256);  // row-split: one group reads a slot
       mbar_init(&o_full[s], 1);
+      mbar_init(&o_free[s], 128);
     }
     for (int s = 0; s < 4; ++s) {
       mbar_init(&p_full[s], 128);
@@ -385,6 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // from the last P block to O).
         const uint32_t g = warp - 9;
         const uint32_t slot_tmem = tmem + g * 256;
+        const uint32_t o_tmem = slot_tmem + static_cast<uint32_t>(L.o_sep);
         uint32_t j = 0, pu = 0, n = 0, it = 0;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
           const int kvs = ring_slot(it, L.n_kv);
@@ -413,17 +426,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (kOne) umma_commit_w(&kv_free[kvs]);  // this tile's use of K is done
             TRACE(4);
             if (kOne) mbar_wait(&v_full[kvs], kv_par);
+            if (L.o_sep && j > 0) mbar_wait(&o_free[g], (j - 1) & 1);  // O of the previous tile read
             for (int kb = 0; kb < L.n_kb; ++kb) {
               const int ps = 2 * g + (pu & 1);
               mbar_wait(&p_full[ps], (pu >> 1) & 1);
               ++pu;
-              // head_dim 80: O[0, 80) overlaps S block 1, so block 0's PV waits for block 1's P
-              if (kTail > 0 && kb == 0 && L.n_kb > 1) mbar_wait(&p_full[2 * g + (pu & 1)], (pu >> 1) & 1);
+              // head_dim 80 with O in the slot: O[0, 80) overlaps S block 1, so block 0's PV waits
+              // for block 1's P
+              if (kTail > 0 && kb == 0 && L.n_kb > 1 && !L.o_sep)
+                mbar_wait(&p_full[2 * g + (pu & 1)], (pu >> 1) & 1);
               TRACE(8 + 16 * g);
               tc_fence_after();
               const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
               const int nkc = kb == L.n_kb - 1 ? L.nkc_last : kKeyBlk / 16;
-              pv_block(std::true_type{}, slot_tmem, pdesc, sKVslot, kb, nkc);
+              pv_block(std::true_type{}, o_tmem, pdesc, sKVslot, kb, nkc);
               umma_commit_w(&p_free[ps]);
               TRACE(5 + 16 * g);
             }
@@ -648,17 +664,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             TRACE(14);
           }
           const float inv = rcp_approx(f2_total(acc));
+          if (L.o_sep) mbar_arrive(&s_free[g]);  // S read (tc_fence_before above): the next S may go
           // epilogue: O (64 columns of this slot) / sum -> bf16 row
           mbar_wait(&o_full[g], k & 1);
           TRACE(17);
           tc_fence_after();
           uint32_t o0[32], o1[32], ot[16];
-          tmem_ld_32x32b_x32(la, o0);
-          tmem_ld_32x32b_x32(la + 32, o1);
-          if constexpr (kTail > 0) tmem_ld_32x32b_x16(la + kHd, ot);
+          const uint32_t lo = la + static_cast<uint32_t>(L.o_sep);
+          tmem_ld_32x32b_x32(lo, o0);
+          tmem_ld_32x32b_x32(lo + 32, o1);
+          if constexpr (kTail > 0) tmem_ld_32x32b_x16(lo + kHd, ot);
           tmem_ld_wait();
           tc_fence_before();
-          mbar_arrive(&s_free[g]);
+          mbar_arrive(L.o_sep ? &o_free[g] : &s_free[g]);
           const int q0 = qt * kQTile + (warp & 3) * 32;
           if (q0 < t) {
             store_o_slab(&tmo, o0, inv, s_slab, lane, h * kHD, q0, b);
