@@ -457,6 +457,109 @@ __global__ void __launch_bounds__(256)
         lane == 0 ? make_float2(s_all, q_all) : make_float2(0.f, 0.f);
 }
 
+// merge_fixup, one CTA per image with one warp per source (r <= 32): every warp loads its
+// source row (scaled by its size) into shared memory and, if it is its destination's first
+// source, the destination row, all at once; after one barrier the first-source warp adds
+// self, then the sources by rank (merge_kernel's order) -- one dependent global round trip
+// instead of a chain of them.  Block-wide: the new size vector.
+template <int VEC>
+__global__ void __launch_bounds__(1024)
+    merge_fixup_par_kernel(float* __restrict__ x_out, const float* __restrict__ side,
+                           const float* __restrict__ size, float* __restrict__ size_out, int t, int r,
+                           const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                           const int32_t* __restrict__ unm, __nv_bfloat16* __restrict__ xh,
+                           float* __restrict__ stats) {
+  constexpr int D = 128 * VEC;
+  extern __shared__ float4 s_rows[];  // [r][D / 4]: s_k x_k of source k
+  __shared__ int s_src[32];
+  __shared__ int s_dst[32];
+  __shared__ float s_ssz[32];  // size of source k
+  const int b = blockIdx.x;
+  const int na = (t + 1) / 2, n_unm = na - r, tp = t - r;
+  const int k = warp_id(), lane = lane_id();
+  grid_dep_wait();
+  grid_dep_launch();
+  // this warp's source and destination (every lane reads the same words: one broadcast)
+  const int sk = src[static_cast<long long>(b) * r + k];
+  const int j = dst[static_cast<long long>(b) * r + k];
+  const float ss = size != nullptr ? size[static_cast<long long>(b) * t + 2 * sk] : 1.0f;
+  if (lane == 0) {
+    s_src[k] = sk;
+    s_dst[k] = j;
+    s_ssz[k] = ss;
+  }
+  const float4* sr = reinterpret_cast<const float4*>(side + (static_cast<long long>(b) * r + k) * D);
+  float4 v[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) v[i] = sr[lane + 32 * i];
+  __syncthreads();  // s_dst complete
+  bool first = true;
+  for (int q = 0; q < k; ++q) first = first && s_dst[q] != j;
+  const long long orow = static_cast<long long>(b) * tp + n_unm + j;
+  float4 acc[VEC];
+  float s_d = 0.f;
+  if (first) {  // the destination row, loaded beside the source row
+    s_d = size != nullptr ? size[static_cast<long long>(b) * t + 2 * j + 1] : 1.0f;
+    const float4* xr = reinterpret_cast<const float4*>(x_out + orow * D);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) acc[i] = xr[lane + 32 * i];
+  }
+#pragma unroll
+  for (int i = 0; i < VEC; ++i)
+    s_rows[k * (D / 4) + lane + 32 * i] = make_float4(v[i].x * ss, v[i].y * ss, v[i].z * ss, v[i].w * ss);
+  // new sizes: unmerged A tokens keep theirs, B tokens add their sources' (rank order)
+  for (int o = threadIdx.x; o < tp; o += blockDim.x) {
+    float stot;
+    if (o < n_unm) {
+      const int tok = 2 * unm[static_cast<long long>(b) * n_unm + o];
+      stot = size != nullptr ? size[static_cast<long long>(b) * t + tok] : 1.0f;
+    } else {
+      const int jj = o - n_unm;
+      stot = size != nullptr ? size[static_cast<long long>(b) * t + 2 * jj + 1] : 1.0f;
+      for (int q = 0; q < r; ++q)
+        if (s_dst[q] == jj) stot += s_ssz[q];
+    }
+    size_out[static_cast<long long>(b) * tp + o] = stot;
+  }
+  __syncthreads();  // every source row staged
+  if (!first) return;
+  float stot = s_d;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) acc[i] = make_float4(acc[i].x * s_d, acc[i].y * s_d, acc[i].z * s_d, acc[i].w * s_d);
+  for (int q = k; q < r; ++q) {
+    if (s_dst[q] != j) continue;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      const float4 w = s_rows[q * (D / 4) + lane + 32 * i];
+      acc[i].x += w.x;
+      acc[i].y += w.y;
+      acc[i].z += w.z;
+      acc[i].w += w.w;
+    }
+    stot += s_ssz[q];
+  }
+  float sum = 0.f, q2 = 0.f;
+  float4* xr = reinterpret_cast<float4*>(x_out + orow * D);
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    acc[i].x /= stot;
+    acc[i].y /= stot;
+    acc[i].z /= stot;
+    acc[i].w /= stot;
+    sum += (acc[i].x + acc[i].y) + (acc[i].z + acc[i].w);
+    q2 += (acc[i].x * acc[i].x + acc[i].y * acc[i].y) + (acc[i].z * acc[i].z + acc[i].w * acc[i].w);
+    xr[lane + 32 * i] = acc[i];
+    uint2 p;
+    p.x = pack_bf16(acc[i].x, acc[i].y);
+    p.y = pack_bf16(acc[i].z, acc[i].w);
+    *reinterpret_cast<uint2*>(xh + orow * D + 4 * (lane + 32 * i)) = p;
+  }
+  const float s_all = warp_sum(sum), q_all = warp_sum(q2);
+  if (lane < VEC)  // whole-row sums in slot 0, the other 128-column slots zero
+    *reinterpret_cast<float2*>(stats + 2 * (orow * VEC + lane)) =
+        lane == 0 ? make_float2(s_all, q_all) : make_float2(0.f, 0.f);
+}
+
 static cudaLaunchConfig_t pdl_cfg(dim3 grid, cudaStream_t s, cudaLaunchAttribute* attr) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
@@ -478,10 +581,50 @@ int merge_map(const int32_t* src, const int32_t* unm, int B, int t, int r, int32
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 
+static int fixup_backend() {  // profiling: TA_FIXUP=chain keeps the per-source-chain kernel
+  static int mode = -1;
+  if (mode < 0) {
+    const char* v = getenv("TA_FIXUP");
+    mode = (v && v[0] == 'c') ? 1 : 0;
+  }
+  return mode;
+}
+
 int merge_fixup(float* x_out, const float* side, const float* size, float* size_out, int B, int t,
                 int D, int r, const int32_t* src, const int32_t* dst, const int32_t* unm, void* xh,
                 float* stats, cudaStream_t s) {
   if (r <= 0 || r > (t + 1) / 2 - 1 || r > 256 || t > 1024) return TA_ERR_INVALID;
+  if (r <= 32 && fixup_backend() == 0) {
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = pdl_cfg(dim3(B), s, attr);
+    cfg.blockDim = dim3(32 * r);
+    cfg.dynamicSmemBytes = static_cast<size_t>(r) * D * sizeof(float);
+    auto* h = static_cast<__nv_bfloat16*>(xh);
+    cudaError_t e;
+    switch (D) {
+#define TA_FIXUP_PAR_CASE(DIM, V)                                                                       \
+  case DIM: {                                                                                           \
+    static unsigned long long attr_mask = 0;                                                            \
+    if (attr_needed(attr_mask)) {                                                                       \
+      e = cudaFuncSetAttribute(merge_fixup_par_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                               32 * DIM * 4);                                                           \
+      if (e != cudaSuccess) return set_last_cuda_error(e);                                              \
+      attr_done(attr_mask);                                                                             \
+    }                                                                                                   \
+    e = cudaLaunchKernelEx(&cfg, merge_fixup_par_kernel<V>, x_out, side, size, size_out, t, r, src, dst, \
+                           unm, h, stats);                                                              \
+    break;                                                                                              \
+  }
+      TA_FIXUP_PAR_CASE(256, 2)
+      TA_FIXUP_PAR_CASE(768, 6)
+      TA_FIXUP_PAR_CASE(1024, 8)
+      TA_FIXUP_PAR_CASE(1280, 10)
+#undef TA_FIXUP_PAR_CASE
+      default:
+        return TA_ERR_SHAPE;
+    }
+    return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+  }
   cudaLaunchAttribute attr[1];
   const cudaLaunchConfig_t cfg = pdl_cfg(dim3(B, (r + 7) / 8), s, attr);
   auto* h = static_cast<__nv_bfloat16*>(xh);
