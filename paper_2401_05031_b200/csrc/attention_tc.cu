@@ -382,7 +382,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
           const int nkc = kb == L.n_kb - 1 ? L.nkc_last : kKeyBlk / 16;
+#ifndef TA_ATTN_EXP_NOPV  // profiling only: wrong results (key-split PV MMAs skipped)
           pv_block(std::true_type{}, o_tmem, pdesc, sKVslot, kb, nkc);
+#endif
           umma_commit_w(&p_free[ps]);
         }
         umma_commit_w(&o_full[sslot]);
