@@ -28,5 +28,6 @@ for gamma in (-16, -8):
     replay = bb.forward_raw(imgs, ids, gamma, forced_trace=trace.clone())
     torch.cuda.synchronize()
     torch.save({"out": out.cpu(), "forced": forced.cpu(), "trace": trace.cpu(), "replay": replay.cpu()},
-               os.path.join(sys.argv[1], f"fusion{os.environ.get('TA_MERGE_FUSION', '0')}_g{gamma}.pt"))
+               os.path.join(sys.argv[1], f"fusion{os.environ.get('TA_MERGE_FUSION', '0')}"
+                                         f"{'c' if os.environ.get('TA_FIXUP') == 'chain' else ''}_g{gamma}.pt"))
 print("ok")

@@ -191,14 +191,15 @@ def test_merge_fusion_matches_merge_kernel(tmp_path):
     """The fused proj + merge path (TA_MERGE_FUSION=1, the bf16 default) and the separate merge
     kernel (TA_MERGE_FUSION=0) give, with the same forced trace, logits within the bf16 bound of
     each other; each path replays its own free-running trace bit for bit (fused: the match
-    kernel's row map = merge_map's)."""
+    kernel's row map = merge_map's); the fused path's fixup kernels (one warp per source, and
+    the per-source chain with TA_FIXUP=chain) agree within the bf16 bound."""
     import os
     import subprocess
     import sys
 
     here = os.path.dirname(os.path.abspath(__file__))
-    for flag in ("0", "1"):
-        env = dict(os.environ, TA_MERGE_FUSION=flag)
+    for flag, fixup in (("0", ""), ("1", ""), ("1", "chain")):
+        env = dict(os.environ, TA_MERGE_FUSION=flag, TA_FIXUP=fixup)
         r = subprocess.run([sys.executable, os.path.join(here, "merge_fusion_check.py"), str(tmp_path)],
                            env=env, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
@@ -213,3 +214,6 @@ def test_merge_fusion_matches_merge_kernel(tmp_path):
         assert a["trace"].shape == b["trace"].shape and (b["trace"] >= 0).all()
         for run in (a, b):
             assert torch.equal(run["out"], run["replay"])
+        # the one-warp-per-source fixup against the per-source chain kernel, same forced trace
+        c = torch.load(tmp_path / f"fusion1c_g{gamma}.pt")
+        assert (fb - _finite(c["forced"])).abs().max().item() <= BF16_TOL * scale
