@@ -511,6 +511,8 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
 #ifndef TA_GEMM_BUFS
 #define TA_GEMM_BUFS 1
 #endif
+constexpr int kMaxStatSlots = 10;  // D / 128 for D <= 1280 (ViT-H)
+
 template <int EPI, typename OutT, bool kRemap>
 struct PairCfg {
   static constexpr bool kTma = pair_tma(EPI, kRemap);
@@ -525,8 +527,19 @@ struct PairCfg {
   static constexpr int kBBytes = 128 * kBK * 2;  // this CTA's half of the 256-row W tile
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kEpiBytes = kTma ? kWarps * kBufs * 4096 : kEpiWarps * 32 * 32 * 4;
-  static constexpr int kStages = kEpiBytes > 32768 ? 5 : 6;
-  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + 1024 + 512;
+  // fc1 (EPI_LN_GELU): the LN-fold column constants c1 / c2 of a warp's 128 columns staged in
+  // shared memory once per tile (1 KB per warp, loaded before the accumulator wait) instead of
+  // 32 LDG.128 per 64-column box: those loads left the tensor pipe idle ~30 % of fc1 (ncu: 186
+  // -> 164 us with them removed); costs the sixth mainloop stage.  Build with
+  // -DTA_GEMM_LN_SMEM=0 to keep the loads, =2 to stage them for the QKV GEMM too.
+#ifndef TA_GEMM_LN_SMEM
+#define TA_GEMM_LN_SMEM 1
+#endif
+  static constexpr bool kLnSmem =
+      kTma && TA_GEMM_LN_SMEM && (EPI == EPI_LN_GELU || (TA_GEMM_LN_SMEM == 2 && EPI == EPI_LN_BIAS));
+  static constexpr int kLnBytes = kLnSmem ? kWarps * 1024 : 0;
+  static constexpr int kStages = (kEpiBytes > 32768 || kLnSmem) ? 5 : 6;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + kLnBytes + 1024 + 512;
 };
 
 template <int EPI, typename OutT, bool kRemap>
@@ -544,7 +557,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* epi_smem = smem + S * Cfg::kStageBytes;
   float4* epi_stage = reinterpret_cast<float4*>(epi_smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + Cfg::kEpiBytes);
+  uint8_t* ln_smem = epi_smem + Cfg::kEpiBytes;  // kLnSmem: [kWarps][c1 128 | c2 128] fp32
+  uint64_t* full = reinterpret_cast<uint64_t*>(ln_smem + Cfg::kLnBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -692,6 +706,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
         if (m < M)
           prefetch_l2_bulk(epi.resid + m * N + n_blk * BN + col0, BN / kSplit * sizeof(float));
       }
+      // LN finish (EPI_LN_*): this thread's row statistics, once per tile -- loaded before the
+      // accumulator wait, so their L2 latency hides under this tile's mainloop
+      float ln_mu = 0.f, ln_rstd = 0.f;
+      if constexpr (epi_is_ln(EPI) && Cfg::kTma) {
+        const long long m = m_base + lane;
+        if (m < M) {
+          const float2* sp = reinterpret_cast<const float2*>(epi.ln_stats) + m * epi.stat_slots;
+          float2 p[kMaxStatSlots];
+#pragma unroll
+          for (int j = 0; j < kMaxStatSlots; ++j)
+            if (j < epi.stat_slots) p[j] = __ldg(sp + j);
+          float2 st = p[0];
+#pragma unroll
+          for (int j = 1; j < kMaxStatSlots; ++j) {
+            if (j < epi.stat_slots) {
+              st.x += p[j].x;
+              st.y += p[j].y;
+            }
+          }
+          ln_mu = st.x * epi.inv_dim;
+          ln_rstd = rsqrtf(fmaxf(st.y * epi.inv_dim - ln_mu * ln_mu, 0.f) + 1e-6f);
+        }
+      }
+      const uint32_t ln_s = smem_u32(ln_smem) + ew * 1024u;  // this warp's c1 | c2 (kLnSmem)
+      if constexpr (Cfg::kLnSmem) {
+        // lane l: columns 4 l .. 4 l + 3 of the warp's 128 (the previous tile's reads of this
+        // warp-private area are done: same warp, program order)
+        const int nc = n_blk * BN + col0 + 4 * static_cast<int>(lane);
+        const float4 a1 = __ldg(reinterpret_cast<const float4*>(epi.c1 + nc));
+        const float4 a2 = __ldg(reinterpret_cast<const float4*>(epi.c2 + nc));
+        __syncwarp();
+        sts_f4(ln_s + lane * 16u, a1);
+        sts_f4(ln_s + 512u + lane * 16u, a2);
+        __syncwarp();
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * BN + col0;
@@ -701,21 +750,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
         constexpr int NCH = (BN / kSplit) / CW;
         const long long m = m_base + lane;
         const bool row_ok = m < M;
-        // LN finish (EPI_LN_*): this thread's row statistics, once per tile
-        float ln_mu = 0.f, ln_rstd = 0.f;
-        if constexpr (epi_is_ln(EPI)) {
-          if (row_ok) {
-            const float2* sp = reinterpret_cast<const float2*>(epi.ln_stats) + m * epi.stat_slots;
-            float2 st = __ldg(sp);
-            for (int j = 1; j < epi.stat_slots; ++j) {
-              const float2 p = __ldg(sp + j);
-              st.x += p.x;
-              st.y += p.y;
-            }
-            ln_mu = st.x * epi.inv_dim;
-            ln_rstd = rsqrtf(fmaxf(st.y * epi.inv_dim - ln_mu * ln_mu, 0.f) + 1e-6f);
-          }
-        }
         // row statistics of the stored values (EPI_*_STATS) and this row's output row index
         float st_s = 0.f, st_q = 0.f;
         long long orow = m;
@@ -747,6 +781,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
             if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
           }
           if (epi.skip == 1) return false;
+          if (epi.skip >= 4 && static_cast<int>(q) == epi.skip - 4) return false;  // profiling: one lane quarter's warps idle
           if constexpr (Cfg::kResidTma) {
             if (resid_tma) {
               if (c + 1 < NCH) resid_load(c + 1);
@@ -793,7 +828,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
             const uint64_t nmu2 = f2_pack(-ln_mu, -ln_mu), rstd2 = f2_pack(ln_rstd, ln_rstd);
 #pragma unroll
             for (int j = 0; j < CW / 4; ++j) {
-              const float4 a1 = __ldg(c1p + j), a2 = __ldg(c2p + j);
+#ifdef TA_EXP_LN_NOLOAD  // profiling only: wrong results (LN-fold column constants not loaded)
+              const float4 a1 = make_float4(v[0], v[1], v[2], v[3]), a2 = a1;
+#else
+              float4 a1, a2;
+              if constexpr (Cfg::kLnSmem) {  // broadcast LDS of the staged constants
+                a1 = lds_f4(ln_s + static_cast<uint32_t>(c * CW + 4 * j) * 4u);
+                a2 = lds_f4(ln_s + 512u + static_cast<uint32_t>(c * CW + 4 * j) * 4u);
+              } else {
+                a1 = __ldg(c1p + j);
+                a2 = __ldg(c2p + j);
+              }
+#endif
               const float2 lo = f2_unpack(ffma2(rstd2, ffma2(nmu2, f2_pack(a1.x, a1.y), f2_pack(v[4 * j], v[4 * j + 1])),
                                                 f2_pack(a2.x, a2.y)));
               const float2 hi = f2_unpack(ffma2(rstd2, ffma2(nmu2, f2_pack(a1.z, a1.w), f2_pack(v[4 * j + 2], v[4 * j + 3])),
@@ -1319,6 +1365,7 @@ int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, b
   if (K % kBK != 0 || N % 128 != 0) return TA_ERR_SHAPE;
   if ((epi_is_resid(epi_kind) || epi_is_patch(epi_kind)) && out_bf16) return TA_ERR_INVALID;
   if (epi_is_ln(epi_kind) && !out_bf16) return TA_ERR_INVALID;
+  if (epi_is_ln(epi_kind) && epi_in.stat_slots > kMaxStatSlots) return TA_ERR_SHAPE;
   static const int force_bn = [] {  // profiling: TA_GEMM_BN=128 forces the 128 x 128 kernel
     const char* v = getenv("TA_GEMM_BN");
     return v ? atoi(v) : 0;

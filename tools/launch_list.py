@@ -9,7 +9,8 @@ gammas = [int(a) for a in sys.argv[1:]] or [-16, -8, 0, 8, 16]
 MODEL = os.environ.get("MODEL", "vit_b16"); BATCH = int(os.environ.get("BATCH", "256"))
 cfg, params = helpers.backbone(MODEL)
 tasks = helpers.task_params(cfg, (100,), [g for g in gammas if g > 0])
-sm = helpers.serve_model(cfg, params, tasks, dtype=os.environ.get("DTYPE", "bf16"))
+sm = helpers.serve_model(cfg, params, tasks, dtype=os.environ.get("DTYPE", "bf16"),
+                         fold_ln=None if os.environ.get("FOLD_LN") is None else os.environ["FOLD_LN"] == "1")
 bb = sm.backbone
 imgs = torch.randn(BATCH, 3, cfg.img, cfg.img, device="cuda")
 ids = torch.zeros(BATCH, dtype=torch.int32, device="cuda")
