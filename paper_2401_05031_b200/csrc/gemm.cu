@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
 #endif
 constexpr int kMaxStatSlots = 10;  // D / 128 for D <= 1280 (ViT-H)
 
-template <int EPI, typename OutT, bool kRemap>
+template <int EPI, typename OutT, bool kRemap, bool kXhTma = false>
 struct PairCfg {
   static constexpr bool kTma = pair_tma(EPI, kRemap);
   // (16 epilogue warps with one box each measured slower than 8 with two: register spills)
@@ -538,18 +538,25 @@ struct PairCfg {
   static constexpr bool kLnSmem =
       kTma && TA_GEMM_LN_SMEM && (EPI == EPI_LN_GELU || (TA_GEMM_LN_SMEM == 2 && EPI == EPI_LN_BIAS));
   static constexpr int kLnBytes = kLnSmem ? kWarps * 1024 : 0;
-  static constexpr int kStages = (kEpiBytes > 32768 || kLnSmem) ? 5 : 6;
-  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + kLnBytes + 1024 + 512;
+  // Short-K residual + statistics GEMM (proj; gemm_bf16 picks K <= 1024): the bf16 copy of the
+  // output rows leaves by TMA too, from two 2 KB staging boxes per warp (32 rows x 64 bytes,
+  // SW64) instead of two thread-per-row STG.256 per box (ncu: those stores and the statistics
+  // were 19 % of proj; 86.5 -> 83.0 us); its mainloop (12 k-blocks) runs on 4 stages.
+  static constexpr bool kXh = kXhTma && kResidTma && epi_is_stats(EPI) && !kRemap;
+  static constexpr int kXhBytes = kXh ? kWarps * 2 * 2048 : 0;
+  static constexpr int kStages = kXh ? 4 : (kEpiBytes > 32768 || kLnSmem) ? 5 : 6;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + kLnBytes + kXhBytes + 1024 + 512;
 };
 
-template <int EPI, typename OutT, bool kRemap>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, kRemap>::kThreads, 1)
+template <int EPI, typename OutT, bool kRemap, bool kXhTma>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, kRemap, kXhTma>::kThreads, 1)
     gemm_bf16_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                                 const __grid_constant__ CUtensorMap tmB,
                                 const __grid_constant__ CUtensorMap tmC,
-                                const __grid_constant__ CUtensorMap tmR, int M, int N, int K,
+                                const __grid_constant__ CUtensorMap tmR,
+                                const __grid_constant__ CUtensorMap tmX, int M, int N, int K,
                                 GemmEpi epi) {
-  using Cfg = PairCfg<EPI, OutT, kRemap>;
+  using Cfg = PairCfg<EPI, OutT, kRemap, kXhTma>;
   constexpr int BN = 256;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -558,7 +565,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
   uint8_t* epi_smem = smem + S * Cfg::kStageBytes;
   float4* epi_stage = reinterpret_cast<float4*>(epi_smem);
   uint8_t* ln_smem = epi_smem + Cfg::kEpiBytes;  // kLnSmem: [kWarps][c1 128 | c2 128] fp32
-  uint64_t* full = reinterpret_cast<uint64_t*>(ln_smem + Cfg::kLnBytes);
+  uint8_t* xh_smem = ln_smem + Cfg::kLnBytes;     // kXh: [kWarps][2] 32 x 64-byte bf16 boxes
+  uint64_t* full = reinterpret_cast<uint64_t*>(xh_smem + Cfg::kXhBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -575,6 +583,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
     tma_prefetch(&tmB);
     if constexpr (Cfg::kTma) tma_prefetch(&tmC);
     if constexpr (Cfg::kResidTma) tma_prefetch(&tmR);
+    if constexpr (Cfg::kXh) tma_prefetch(&tmX);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < S; ++s) {
@@ -763,7 +772,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
         const bool keep_row = row_ok && (!kMerge || orow < epi.rows_out);
         // compute(c): TMEM columns of box c -> bias / LN / GELU / residual -> 8 packed 16-byte
         // words of this thread's row (w); stage_store(c, w): swizzled staging box + TMA store.
-        auto compute = [&](int c, uint4 (&w)[8]) -> bool {
+        auto compute = [&](int c, uint4 (&w)[8], uint4 (&xw)[4]) -> bool {
           const int n0 = n_blk * BN + col0 + c * CW;
           float v[CW];
           {
@@ -872,16 +881,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           }
           if constexpr (epi_is_stats(EPI)) {
             // bf16 copy of the stored row chunk (next GEMM's A operand) + row statistics
+            if constexpr (Cfg::kXh) {  // packed here, staged and stored by TMA in stage_store
+              static_assert(CW == 32, "fp32 boxes: 32 columns of bf16 copy");
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                xw[j] = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                                   pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+            }
             if (keep_row) {
               uint4* xr = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.xh) + orow * N + n0);
               static_assert(CW % 16 == 0, "32-byte xh stores");
 #pragma unroll
               for (int j = 0; j < CW / 16; ++j)  // full 32-byte sectors (STG.256)
-                stg256(xr + 2 * j,
-                       make_uint4(pack_bf16(v[16 * j], v[16 * j + 1]), pack_bf16(v[16 * j + 2], v[16 * j + 3]),
-                                  pack_bf16(v[16 * j + 4], v[16 * j + 5]), pack_bf16(v[16 * j + 6], v[16 * j + 7])),
-                       make_uint4(pack_bf16(v[16 * j + 8], v[16 * j + 9]), pack_bf16(v[16 * j + 10], v[16 * j + 11]),
-                                  pack_bf16(v[16 * j + 12], v[16 * j + 13]), pack_bf16(v[16 * j + 14], v[16 * j + 15])));
+                if (!Cfg::kXh || (!kRemap && epi.direct_store))
+                  stg256(xr + 2 * j,
+                         make_uint4(pack_bf16(v[16 * j], v[16 * j + 1]), pack_bf16(v[16 * j + 2], v[16 * j + 3]),
+                                    pack_bf16(v[16 * j + 4], v[16 * j + 5]), pack_bf16(v[16 * j + 6], v[16 * j + 7])),
+                         make_uint4(pack_bf16(v[16 * j + 8], v[16 * j + 9]), pack_bf16(v[16 * j + 10], v[16 * j + 11]),
+                                    pack_bf16(v[16 * j + 12], v[16 * j + 13]), pack_bf16(v[16 * j + 14], v[16 * j + 15])));
               uint64_t s2 = 0ull, q2 = 0ull;  // packed partial sums (two chains)
 #pragma unroll
               for (int j = 0; j < CW; j += 2) {
@@ -906,7 +923,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           }
           return true;
         };
-        auto stage_store = [&](int c, const uint4 (&w)[8]) {
+        auto stage_store = [&](int c, const uint4 (&w)[8], const uint4 (&xw)[4]) {
           const int n0 = n_blk * BN + col0 + c * CW;
           if (Cfg::kResidTma && resid_tma) tma_buf = c & 1;  // the residual's box (already free)
           uint8_t* sbuf = epi_smem + (ew * Cfg::kBufs + tma_buf) * 4096;
@@ -934,6 +951,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
             sts_u4(srow + ((j ^ (lane & 7)) << 4), w[j]);
             if (kRemap && spill_row != nullptr) spill_row[j] = w[j];
           }
+          // bf16 copy box c & 1 (its previous store, box c - 2, was waited for by resid_load)
+          const uint32_t xbox = smem_u32(xh_smem) + (ew * 2u + static_cast<uint32_t>(c & 1)) * 2048u;
+          if constexpr (Cfg::kXh) {
+            if (!resid_tma) {  // (the per-thread residual path does not wait in resid_load)
+              if (lane == 0) bulk_wait_group_read<0>();
+              __syncwarp();
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)  // SW64: 16-byte chunk j of row r at j ^ ((r >> 1) & 3)
+              sts_u4(xbox + lane * 64u + ((j ^ ((lane >> 1) & 3)) << 4), xw[j]);
+          }
           fence_proxy_async_shared();
           __syncwarp();
           if constexpr (kMerge) {
@@ -943,7 +971,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
             for (int g = 0; g < 8; ++g) {
               const int r0 = __shfl_sync(0xffffffffu, dst, 4 * g), r1 = __shfl_sync(0xffffffffu, dst, 4 * g + 1);
               const int r2 = __shfl_sync(0xffffffffu, dst, 4 * g + 2), r3 = __shfl_sync(0xffffffffu, dst, 4 * g + 3);
-              if (lane == 0 && epi.skip != 2) tma_scatter4(&tmC, smem_u32(sbuf) + g * 512, n0, r0, r1, r2, r3);
+              if (lane == 0 && epi.skip != 2) {
+                tma_scatter4(&tmC, smem_u32(sbuf) + g * 512, n0, r0, r1, r2, r3);
+                if constexpr (Cfg::kXh) tma_scatter4(&tmX, xbox + g * 256, n0, r0, r1, r2, r3);
+              }
             }
             if (lane == 0 && epi.skip != 2) bulk_commit_group();
           } else if (lane == 0 && epi.skip != 2) {
@@ -954,6 +985,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
               tma_store_3d(&tmC, sbuf, n0, epi.row_off + i0, b);
             } else {
               tma_store_2d(&tmC, sbuf, n0, static_cast<int32_t>(m_base));
+              if constexpr (Cfg::kXh) tma_store_2d_s(&tmX, xbox, n0, static_cast<int32_t>(m_base));
             }
             bulk_commit_group();
           }
@@ -973,12 +1005,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
         };
 #pragma unroll 1
         for (int c = 0; c < NCH; ++c) {
-          uint4 w[8];
-          if (compute(c, w)) {
+          uint4 w[8], xw[4];
+          if (compute(c, w, xw)) {
             if (!kRemap && epi.direct_store)
               direct_store(c, w);
             else
-              stage_store(c, w);
+              stage_store(c, w, xw);
           }
         }
         if constexpr (epi_is_stats(EPI)) {
@@ -1203,6 +1235,20 @@ static int make_tmap_out(CUtensorMap* map, const void* base, uint64_t rows, uint
   return r == CUDA_SUCCESS ? TA_OK : TA_ERR_SHAPE;
 }
 
+// bf16 copy of a residual kind's output: 32-column (64-byte) boxes, SW64.
+static int make_tmap_xh(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  auto enc = get_encode_fn();
+  if (!enc) return TA_ERR_CUDA;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? TA_OK : TA_ERR_SHAPE;
+}
+
 // 3D view [B][rows_out][N] of a row-remapped output, same 32-row x 128-byte boxes.
 static int make_tmap_out3(CUtensorMap* map, const void* base, uint64_t images, uint64_t rows_out,
                           uint64_t cols, bool bf16) {
@@ -1236,11 +1282,11 @@ int make_tmap_attn_out(CUtensorMap* map, const void* base, uint64_t images, uint
   return r == CUDA_SUCCESS ? TA_OK : TA_ERR_SHAPE;
 }
 
-template <int EPI, typename OutT, bool kRemap = false>
+template <int EPI, typename OutT, bool kRemap = false, bool kXhTma = false>
 static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, int N, int K,
                        const GemmEpi& epi, cudaStream_t stream) {
-  using Cfg = PairCfg<EPI, OutT, kRemap>;
-  auto kern = gemm_bf16_sm100_pair_kernel<EPI, OutT, kRemap>;
+  using Cfg = PairCfg<EPI, OutT, kRemap, kXhTma>;
+  auto kern = gemm_bf16_sm100_pair_kernel<EPI, OutT, kRemap, kXhTma>;
   static unsigned long long attr_mask = 0;  // per instantiation and device
   if (attr_needed(attr_mask)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1259,6 +1305,11 @@ static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
     const int rc = make_tmap_out(&tr_, epi.resid, M, N, false);
     if (rc) return rc;
   }
+  CUtensorMap tx_{};
+  if (Cfg::kXh) {  // bf16 copy: 32-column (64-byte, SW64) boxes of 32 rows, or single rows to scatter
+    const int rc = make_tmap_xh(&tx_, epi.xh, M, N, EPI == EPI_BIAS_RESID_MERGE ? 1 : 32);
+    if (rc) return rc;
+  }
   const int tiles = ((M + 255) / 256) * (N / 256);
   const int pairs = device_sm_count() / 2;
   cudaLaunchConfig_t cfg = {};
@@ -1271,8 +1322,19 @@ static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta_, tb_, tc_, tr_, M, N, K, epi);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta_, tb_, tc_, tr_, tx_, M, N, K, epi);
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+}
+
+// Residual + statistics GEMMs with K <= kShortK (proj, fused proj + merge) store the bf16 copy
+// by TMA (PairCfg::kXh); TA_GEMM_XH=stg keeps the per-thread stores (A/B).
+constexpr int kShortK = 1024;
+static bool xh_tma_enabled() {
+  static const int on = [] {
+    const char* v = getenv("TA_GEMM_XH");
+    return (v && v[0] == 's') ? 0 : 1;
+  }();
+  return on != 0;
 }
 
 static int dispatch_pair(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
@@ -1290,8 +1352,10 @@ static int dispatch_pair(const CUtensorMap& a, const CUtensorMap& b, int M, int 
     case EPI_PATCH:
       return launch_pair<EPI_PATCH, float, true>(a, b, M, N, K, epi, s);
     case EPI_BIAS_RESID_STATS:
-      return epi.rows_in ? launch_pair<EPI_BIAS_RESID_STATS, float, true>(a, b, M, N, K, epi, s)
-                         : launch_pair<EPI_BIAS_RESID_STATS, float, false>(a, b, M, N, K, epi, s);
+      if (epi.rows_in) return launch_pair<EPI_BIAS_RESID_STATS, float, true>(a, b, M, N, K, epi, s);
+      return K <= kShortK && xh_tma_enabled()
+                 ? launch_pair<EPI_BIAS_RESID_STATS, float, false, true>(a, b, M, N, K, epi, s)
+                 : launch_pair<EPI_BIAS_RESID_STATS, float, false>(a, b, M, N, K, epi, s);
     case EPI_PATCH_STATS:
       return launch_pair<EPI_PATCH_STATS, float, true>(a, b, M, N, K, epi, s);
     case EPI_LN_BIAS:
@@ -1299,6 +1363,8 @@ static int dispatch_pair(const CUtensorMap& a, const CUtensorMap& b, int M, int 
     case EPI_LN_GELU:
       return launch_pair<EPI_LN_GELU, __nv_bfloat16>(a, b, M, N, K, epi, s);
     case EPI_BIAS_RESID_MERGE:
+      // (the merge kind keeps the per-thread bf16 stores: 16 scatter4 per box on a 4-stage ring
+      // measured 81.5 -> 87.5 us per fused proj)
       return launch_pair<EPI_BIAS_RESID_MERGE, float, false>(a, b, M, N, K, epi, s);
   }
   return TA_ERR_INVALID;

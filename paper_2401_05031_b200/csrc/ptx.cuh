@@ -261,6 +261,13 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
       "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d_s(const CUtensorMap* map, uint32_t saddr, int32_t x,
+                                               int32_t y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(saddr), "r"(x), "r"(y)
+               : "memory");
+}
 __device__ __forceinline__ void tma_store_3d_s(const CUtensorMap* map, uint32_t saddr, int32_t x,
                                                int32_t y, int32_t z) {
   asm volatile(
