@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
 #endif
 constexpr int kMaxStatSlots = 10;  // D / 128 for D <= 1280 (ViT-H)
 
-template <int EPI, typename OutT, bool kRemap, bool kXhTma = false>
+template <int EPI, typename OutT, bool kRemap, int kVar = 0>
 struct PairCfg {
   static constexpr bool kTma = pair_tma(EPI, kRemap);
   // (16 epilogue warps with one box each measured slower than 8 with two: register spills)
@@ -521,7 +521,11 @@ struct PairCfg {
   // Residual kinds read the residual through the same staging boxes: TMA loads box c + 1 into
   // the warp's other box while box c is finished (TA_GEMM_RESID=ldg: per-thread row loads).
   static constexpr bool kResidTma = kTma && epi_is_resid(EPI) && sizeof(OutT) == 4;
-  static constexpr int kBufs = kResidTma ? 2 : TA_GEMM_BUFS;  // staging boxes per epilogue warp
+  // kVar 2 (long K: fc2, K >= 2048): one staging box per warp, the next residual box loaded once
+  // this box's store has read it, so the mainloop keeps its sixth stage (a 16 us tile leaves the
+  // epilogue room for the unhidden box loads)
+  static constexpr bool kOneBox = kVar == 2 && kResidTma;
+  static constexpr int kBufs = kOneBox ? 1 : kResidTma ? 2 : TA_GEMM_BUFS;  // staging boxes per epilogue warp
   static constexpr int kThreads = 128 + 32 * kWarps;
   static constexpr int kABytes = 128 * kBK * 2;
   static constexpr int kBBytes = 128 * kBK * 2;  // this CTA's half of the 256-row W tile
@@ -542,21 +546,21 @@ struct PairCfg {
   // output rows leaves by TMA too, from two 2 KB staging boxes per warp (32 rows x 64 bytes,
   // SW64) instead of two thread-per-row STG.256 per box (ncu: those stores and the statistics
   // were 19 % of proj; 86.5 -> 83.0 us); its mainloop (12 k-blocks) runs on 4 stages.
-  static constexpr bool kXh = kXhTma && kResidTma && epi_is_stats(EPI) && !kRemap;
+  static constexpr bool kXh = kVar == 1 && kResidTma && epi_is_stats(EPI) && !kRemap;
   static constexpr int kXhBytes = kXh ? kWarps * 2 * 2048 : 0;
   static constexpr int kStages = kXh ? 4 : (kEpiBytes > 32768 || kLnSmem) ? 5 : 6;
   static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + kLnBytes + kXhBytes + 1024 + 512;
 };
 
-template <int EPI, typename OutT, bool kRemap, bool kXhTma>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, kRemap, kXhTma>::kThreads, 1)
+template <int EPI, typename OutT, bool kRemap, int kVar>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, kRemap, kVar>::kThreads, 1)
     gemm_bf16_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                                 const __grid_constant__ CUtensorMap tmB,
                                 const __grid_constant__ CUtensorMap tmC,
                                 const __grid_constant__ CUtensorMap tmR,
                                 const __grid_constant__ CUtensorMap tmX, int M, int N, int K,
                                 GemmEpi epi) {
-  using Cfg = PairCfg<EPI, OutT, kRemap, kXhTma>;
+  using Cfg = PairCfg<EPI, OutT, kRemap, kVar>;
   constexpr int BN = 256;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -698,7 +702,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
       auto resid_load = [&](int c) {
         if constexpr (Cfg::kResidTma) {
           if (lane == 0) {
-            const int b = c & 1;
+            const int b = Cfg::kOneBox ? 0 : (c & 1);
             bulk_wait_group_read<0>();
             uint64_t* bar = &rfull[ew * Cfg::kBufs + b];
             mbar_arrive_expect_tx(bar, 4096);
@@ -793,8 +797,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           if (epi.skip >= 4 && static_cast<int>(q) == epi.skip - 4) return false;  // profiling: one lane quarter's warps idle
           if constexpr (Cfg::kResidTma) {
             if (resid_tma) {
-              if (c + 1 < NCH) resid_load(c + 1);
-              const int b = c & 1;
+              if (!Cfg::kOneBox && c + 1 < NCH) resid_load(c + 1);
+              const int b = Cfg::kOneBox ? 0 : (c & 1);
               mbar_wait(&rfull[ew * Cfg::kBufs + b], (r_par >> b) & 1u);
               r_par ^= 1u << b;
               // this row's 32 residual values: SW128 chunk j at (j ^ (row & 7))
@@ -925,7 +929,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
         };
         auto stage_store = [&](int c, const uint4 (&w)[8], const uint4 (&xw)[4]) {
           const int n0 = n_blk * BN + col0 + c * CW;
-          if (Cfg::kResidTma && resid_tma) tma_buf = c & 1;  // the residual's box (already free)
+          if (Cfg::kResidTma && resid_tma) tma_buf = Cfg::kOneBox ? 0 : (c & 1);  // the residual's box (already free)
           uint8_t* sbuf = epi_smem + (ew * Cfg::kBufs + tma_buf) * 4096;
           if (!(Cfg::kResidTma && resid_tma) && lane == 0)
             bulk_wait_group_read<Cfg::kBufs - 1>();  // last store from sbuf has read it
@@ -990,6 +994,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
             bulk_commit_group();
           }
           tma_buf = (tma_buf + 1) % Cfg::kBufs;
+          // one box: the next residual box goes into it once this store has read it
+          if constexpr (Cfg::kOneBox)
+            if (resid_tma && c + 1 < NCH) resid_load(c + 1);
         };
         // (Interleaved per box.  Reading every box and releasing the accumulator before any
         // staging wait measured slower: the extra live registers cost more than the wait.)
@@ -1282,11 +1289,11 @@ int make_tmap_attn_out(CUtensorMap* map, const void* base, uint64_t images, uint
   return r == CUDA_SUCCESS ? TA_OK : TA_ERR_SHAPE;
 }
 
-template <int EPI, typename OutT, bool kRemap = false, bool kXhTma = false>
+template <int EPI, typename OutT, bool kRemap = false, int kVar = 0>
 static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, int N, int K,
                        const GemmEpi& epi, cudaStream_t stream) {
-  using Cfg = PairCfg<EPI, OutT, kRemap, kXhTma>;
-  auto kern = gemm_bf16_sm100_pair_kernel<EPI, OutT, kRemap, kXhTma>;
+  using Cfg = PairCfg<EPI, OutT, kRemap, kVar>;
+  auto kern = gemm_bf16_sm100_pair_kernel<EPI, OutT, kRemap, kVar>;
   static unsigned long long attr_mask = 0;  // per instantiation and device
   if (attr_needed(attr_mask)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1329,6 +1336,16 @@ static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
 // Residual + statistics GEMMs with K <= kShortK (proj, fused proj + merge) store the bf16 copy
 // by TMA (PairCfg::kXh); TA_GEMM_XH=stg keeps the per-thread stores (A/B).
 constexpr int kShortK = 1024;
+// Residual GEMMs with K >= kLongK (fc2) use one staging box and keep six stages (PairCfg::kOneBox);
+// TA_GEMM_ONEBOX=0 keeps two boxes (A/B).
+constexpr int kLongK = 2048;
+static bool one_box_enabled() {
+  static const int on = [] {
+    const char* v = getenv("TA_GEMM_ONEBOX");
+    return (v && v[0] == '0') ? 0 : 1;
+  }();
+  return on != 0;
+}
 static bool xh_tma_enabled() {
   static const int on = [] {
     const char* v = getenv("TA_GEMM_XH");
@@ -1347,14 +1364,20 @@ static int dispatch_pair(const CUtensorMap& a, const CUtensorMap& b, int M, int 
       return out_bf16 ? launch_pair<EPI_BIAS_GELU, __nv_bfloat16>(a, b, M, N, K, epi, s)
                       : launch_pair<EPI_BIAS_GELU, float>(a, b, M, N, K, epi, s);
     case EPI_BIAS_RESID:
+      if (K >= kLongK && one_box_enabled())
+        return epi.rows_in ? launch_pair<EPI_BIAS_RESID, float, true, 2>(a, b, M, N, K, epi, s)
+                           : launch_pair<EPI_BIAS_RESID, float, false, 2>(a, b, M, N, K, epi, s);
       return epi.rows_in ? launch_pair<EPI_BIAS_RESID, float, true>(a, b, M, N, K, epi, s)
                          : launch_pair<EPI_BIAS_RESID, float, false>(a, b, M, N, K, epi, s);
     case EPI_PATCH:
       return launch_pair<EPI_PATCH, float, true>(a, b, M, N, K, epi, s);
     case EPI_BIAS_RESID_STATS:
+      if (K >= kLongK && one_box_enabled())
+        return epi.rows_in ? launch_pair<EPI_BIAS_RESID_STATS, float, true, 2>(a, b, M, N, K, epi, s)
+                           : launch_pair<EPI_BIAS_RESID_STATS, float, false, 2>(a, b, M, N, K, epi, s);
       if (epi.rows_in) return launch_pair<EPI_BIAS_RESID_STATS, float, true>(a, b, M, N, K, epi, s);
       return K <= kShortK && xh_tma_enabled()
-                 ? launch_pair<EPI_BIAS_RESID_STATS, float, false, true>(a, b, M, N, K, epi, s)
+                 ? launch_pair<EPI_BIAS_RESID_STATS, float, false, 1>(a, b, M, N, K, epi, s)
                  : launch_pair<EPI_BIAS_RESID_STATS, float, false>(a, b, M, N, K, epi, s);
     case EPI_PATCH_STATS:
       return launch_pair<EPI_PATCH_STATS, float, true>(a, b, M, N, K, epi, s);
