@@ -103,7 +103,7 @@ def _attn_ref(qkv, size, b, t, heads, hd):
     return (s.softmax(-1) @ v).transpose(1, 2).reshape(b, t, heads * hd)
 
 
-@pytest.mark.parametrize("t", [1, 17, 64, 101, 128, 129, 197, 256, 257, 389, 512, 581])
+@pytest.mark.parametrize("t", [1, 17, 64, 101, 128, 129, 197, 256, 257, 300, 384, 389, 512, 581])
 @pytest.mark.parametrize("hd,heads", [(64, 12), (80, 16)])
 @pytest.mark.parametrize("with_size", [False, True])
 @pytest.mark.parametrize("dtype", [0, 1])
@@ -125,7 +125,7 @@ def test_attention(L, t, hd, heads, with_size, dtype):
         torch.testing.assert_close(out.double(), ref, rtol=1e-5, atol=1e-5)
 
 
-@pytest.mark.parametrize("t", [5, 21, 101, 133, 197, 213, 389])
+@pytest.mark.parametrize("t", [5, 21, 101, 133, 197, 213, 261, 341, 389])
 @pytest.mark.parametrize("with_size", [False, True])
 @pytest.mark.parametrize("ramp", [False, True])
 def test_attention_batched_tails(L, t, with_size, ramp):
