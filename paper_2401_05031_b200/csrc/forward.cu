@@ -53,6 +53,19 @@ int merge_fusion_enabled() {
   return on;
 }
 
+// Split-K tail tiles in the forward's GEMMs (gemm.cu splitk_parts), TA_GEMM_SPLITK_FWD=1.  Off by
+// default: a row's fp32 summation order then depends on whether its tile falls in a launch's
+// last wave, so an image's logits would change (in the last bits) with its batch position, and
+// the measured gain is within the sweep's noise.
+static int splitk_fwd_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* v = getenv("TA_GEMM_SPLITK_FWD");
+    on = (v && v[0] == '1') ? 1 : 0;
+  }
+  return on;
+}
+
 int pdl_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -158,6 +171,7 @@ struct Workspace {
   void* tf32_scratch;  // fp32 mode: tf32 hi / lo operand split of the 3xTF32 GEMMs
   int32_t* row_map;  // fused merge: destination of every input row (merge_map); the merged-away
                      // source rows land after the merged rows in x (rows <= B t_max)
+  float* sk_ws;      // bf16 + TA_GEMM_SPLITK_FWD=1: split-K partials + counters, zeroed per forward
   size_t total;
 };
 
@@ -195,12 +209,18 @@ Workspace carve(const ta_model* m, int B, const Schedule& s, char* base) {
                                                         std::max(m->d.mlp_dim, m->kp))
                             : 0);
   w.row_map = reinterpret_cast<int32_t*>(take(r_max > 0 ? rows * 4 : 0));
+  w.sk_ws = m->d.dtype == TA_DTYPE_BF16 && splitk_fwd_enabled()
+                ? reinterpret_cast<float*>(take(gemm_splitk_ws_bytes()))
+                : nullptr;
   w.total = off;
   return w;
 }
 
 int linear(const ta_model* m, const void* a, const void* wt, int M, int N, int K, int epi_kind,
-           const GemmEpi& epi, cudaStream_t st, void* tf32_scratch) {
+           const GemmEpi& epi_in, cudaStream_t st, const Workspace& w) {
+  void* const tf32_scratch = w.tf32_scratch;
+  GemmEpi epi = epi_in;
+  epi.sk_ws = w.sk_ws;
   if (m->d.dtype == TA_DTYPE_BF16)
     return gemm_bf16(a, wt, M, N, K, epi_kind, epi_kind == EPI_BIAS || epi_kind == EPI_BIAS_GELU || epi_is_ln(epi_kind),
                      epi, st);
@@ -465,6 +485,10 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
   if (guard.err != cudaSuccess) return set_last_cuda_error(guard.err);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   StageProfiler prof(st, m);
+  if (w.sk_ws) {  // split-K counters start at zero (each GEMM leaves them zero)
+    cudaError_t me = cudaMemsetAsync(w.sk_ws, 0, gemm_splitk_flag_bytes(), st);
+    if (me != cudaSuccess) return set_last_cuda_error(me);
+  }
   const ta_model_desc& d = m->d;
   const int D = d.dim, L = d.depth, N = m->n_tokens;
   const int act = d.dtype;
@@ -493,7 +517,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
       e.stat_slots = stat_slots;
     }
     TA_TRY(linear(m, w.patches, m->w.patch_w, B * m->n_patches, D, m->kp,
-                  fused ? EPI_PATCH_STATS : EPI_PATCH, e, st, w.tf32_scratch));
+                  fused ? EPI_PATCH_STATS : EPI_PATCH, e, st, w));
     prof.mark(TA_STAGE_PATCH_GEMM, -1);
   }
   TA_TRY(insert_rows(w.x[0], B, s.t[0], D, static_cast<const float*>(m->w.cls),
@@ -525,14 +549,14 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         e.c1 = static_cast<const float*>(Lw.qkv_c1);
         e.c2 = static_cast<const float*>(Lw.qkv_c2);
         e.inv_dim = 1.0f / D;
-        TA_TRY(linear(m, w.h, Lw.qkv_w_ln, M, 3 * D, D, EPI_LN_BIAS, e, st, w.tf32_scratch));
+        TA_TRY(linear(m, w.h, Lw.qkv_w_ln, M, 3 * D, D, EPI_LN_BIAS, e, st, w));
       prof.mark(TA_STAGE_QKV, l);
       } else {
         TA_TRY(layernorm(w.x[cur], static_cast<const float*>(Lw.ln1_w),
                          static_cast<const float*>(Lw.ln1_b), w.h, M, D, act, st));
       prof.mark(TA_STAGE_LN1, l);
         e.bias = static_cast<const float*>(Lw.qkv_b);
-        TA_TRY(linear(m, w.h, Lw.qkv_w, M, 3 * D, D, EPI_BIAS, e, st, w.tf32_scratch));
+        TA_TRY(linear(m, w.h, Lw.qkv_w, M, 3 * D, D, EPI_BIAS, e, st, w));
       prof.mark(TA_STAGE_QKV, l);
       }
     }
@@ -580,16 +604,16 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         e.stat_slots = stat_slots;
         e.row_map = w.row_map;
         e.rows_out = B * (t - r);  // merged rows; the r source rows per image follow them
-        TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID_MERGE, e, st, w.tf32_scratch));
+        TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID_MERGE, e, st, w));
       prof.mark(TA_STAGE_PROJ, l);
       } else if (fused && r == 0) {
         e.xh = w.h;
         e.stats = ln2_stats;
         e.stat_slots = stat_slots;
-        TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID_STATS, e, st, w.tf32_scratch));
+        TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID_STATS, e, st, w));
       prof.mark(TA_STAGE_PROJ, l);
       } else {
-        TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID, e, st, w.tf32_scratch));
+        TA_TRY(linear(m, w.attn, Lw.proj_w, M, D, D, EPI_BIAS_RESID, e, st, w));
       prof.mark(TA_STAGE_PROJ, l);
       }
     }
@@ -626,11 +650,11 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         e.c1 = static_cast<const float*>(Lw.fc1_c1);
         e.c2 = static_cast<const float*>(Lw.fc1_c2);
         e.inv_dim = 1.0f / D;
-        TA_TRY(linear(m, w.h, Lw.fc1_w_ln, Mp, d.mlp_dim, D, EPI_LN_GELU, e, st, w.tf32_scratch));
+        TA_TRY(linear(m, w.h, Lw.fc1_w_ln, Mp, d.mlp_dim, D, EPI_LN_GELU, e, st, w));
       prof.mark(TA_STAGE_FC1, l);
       } else {
         e.bias = static_cast<const float*>(Lw.fc1_b);
-        TA_TRY(linear(m, w.h, Lw.fc1_w, Mp, d.mlp_dim, D, EPI_BIAS_GELU, e, st, w.tf32_scratch));
+        TA_TRY(linear(m, w.h, Lw.fc1_w, Mp, d.mlp_dim, D, EPI_BIAS_GELU, e, st, w));
       prof.mark(TA_STAGE_FC1, l);
       }
     }
@@ -655,7 +679,7 @@ int ta_forward(ta_model* m, const float* images, const int32_t* task_ids, int B,
         e.stat_slots = stat_slots;
       }
       TA_TRY(linear(m, w.mlp, Lw.fc2_w, Mp, D, d.mlp_dim,
-                    stats ? EPI_BIAS_RESID_STATS : EPI_BIAS_RESID, e, st, w.tf32_scratch));
+                    stats ? EPI_BIAS_RESID_STATS : EPI_BIAS_RESID, e, st, w));
       prof.mark(TA_STAGE_FC2, l);
       if (restride) cur ^= 1;
     }
@@ -771,7 +795,18 @@ int ta_gemm(const void* a, const void* w, const float* bias, const float* resid,
   e.resid = resid;
   e.out = out;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (dtype == TA_DTYPE_BF16) return gemm_bf16(a, w, m, n, k, epilogue, out_dtype == TA_DTYPE_BF16, e, st);
+  if (dtype == TA_DTYPE_BF16) {
+    // unit entry point: stream-ordered split-K scratch with zeroed counters
+    void* sk = nullptr;
+    cudaError_t ce = cudaMallocAsync(&sk, gemm_splitk_ws_bytes(), st);
+    if (ce != cudaSuccess) return set_last_cuda_error(ce);
+    ce = cudaMemsetAsync(sk, 0, gemm_splitk_flag_bytes(), st);
+    if (ce != cudaSuccess) return set_last_cuda_error(ce);
+    e.sk_ws = static_cast<float*>(sk);
+    const int rc = gemm_bf16(a, w, m, n, k, epilogue, out_dtype == TA_DTYPE_BF16, e, st);
+    cudaFreeAsync(sk, st);
+    return rc;
+  }
   if (out_dtype != TA_DTYPE_F32) return TA_ERR_INVALID;
   if (f32_gemm_backend() == 0 && k % 32 == 0 && n % 128 == 0) {
     // unit entry point: stream-ordered scratch for the tf32 operand split

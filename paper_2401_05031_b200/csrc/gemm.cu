@@ -552,6 +552,27 @@ struct PairCfg {
   static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + kLnBytes + kXhBytes + 1024 + 512;
 };
 
+// Split-K tail.  When the last wave of 256 x 256 tiles would leave most clusters idle, the
+// launcher cuts each of its R tiles along K into s parts (s <= clusters / R): unit u < full is
+// tile u (full = tiles before the tail), tail unit full + i s + p is part p of tile full + i,
+// k-blocks [p num_kb / s, (p + 1) num_kb / s).  Parts p > 0 store their raw fp32 accumulator to
+// epi.sk_ws (L2) and count one arrival per epilogue warp on a (tile, CTA, warp) counter; part 0,
+// the owner, waits for its counter to reach s - 1, adds the partials in part order (results do
+// not depend on timing), zeroes the counter and runs the tile's epilogue.  Every cluster holds
+// at most one tail unit and it is its last, and the grid is co-resident (one CTA per SM, at
+// most SMs / 2 clusters), so an owner only ever waits on units that are already running.
+struct SkUnit {
+  int tile, kb0, kb1, part, tail;  // tail: index among the split tiles, -1 for full tiles
+};
+__device__ __forceinline__ SkUnit sk_unit(int u, int full, int s, int num_kb) {
+  if (u < full) return {u, 0, num_kb, 0, -1};
+  const int i = u - full, t = i / s, p = i - t * s;
+  return {full + t, p * num_kb / s, (p + 1) * num_kb / s, p, t};
+}
+constexpr int kSkWarpFloats = 32 * 128;  // one epilogue warp's partial: 32 rows x 128 columns
+// scratch layout: counters first (room for 256 tail tiles x 2 CTAs x 8 warps), then partials
+constexpr size_t kSkFlagBytes = 256 * 2 * 8 * 4;
+
 template <int EPI, typename OutT, bool kRemap, int kVar>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, kRemap, kVar>::kThreads, 1)
     gemm_bf16_sm100_pair_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -618,16 +639,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
   const int num_kb = K / kBK;
   const int cid = static_cast<int>(cluster_id_x());
   const int ncl = static_cast<int>(nclusters_x());
+  const int sk_s = epi.sk_split, sk_full = epi.sk_full;
+  const int num_units = sk_full + (num_tiles - sk_full) * sk_s;
 
   if (warp == 0) {
     if (lane == 0) {
       const uint32_t full_leader0 = mapa_shared(&full[0], 0);
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cid; tile < num_tiles; tile += ncl) {
-        const int m_blk = tile / num_n;
-        const int n_blk = tile - m_blk * num_n;
-        for (int kb = 0; kb < num_kb; ++kb) {
+      for (int unit = cid; unit < num_units; unit += ncl) {
+        const SkUnit U = sk_unit(unit, sk_full, sk_s, num_kb);
+        const int m_blk = U.tile / num_n;
+        const int n_blk = U.tile - m_blk * num_n;
+        for (int kb = U.kb0; kb < U.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::kStageBytes;
           uint8_t* sb = sa + Cfg::kABytes;
@@ -652,11 +676,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = cid; tile < num_tiles; tile += ncl) {
+      for (int unit = cid; unit < num_units; unit += ncl) {
+        const SkUnit U = sk_unit(unit, sk_full, sk_s, num_kb);
         mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base_u + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = U.kb0; kb < U.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * Cfg::kStageBytes);
@@ -665,7 +690,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           const uint64_t bdesc = umma_desc_sw128(sb);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
-            umma_f16_pair_w(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            umma_f16_pair_w(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, ((kb - U.kb0) | k) != 0);
           umma_commit_pair_w(&empty[stage]);
           if (++stage == S) {
             stage = 0;
@@ -692,10 +717,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
     int tma_buf = 0;
     uint32_t r_par = 0u;  // kResidTma: bit b = mbarrier parity of staging box b's next load
     const bool resid_tma = Cfg::kResidTma && !epi.resid_ldg;
-    for (int tile = cid; tile < num_tiles; tile += ncl) {
-      const int m_blk = tile / num_n;
-      const int n_blk = tile - m_blk * num_n;
+    for (int unit = cid; unit < num_units; unit += ncl) {
+      const SkUnit U = sk_unit(unit, sk_full, sk_s, num_kb);
+      const int m_blk = U.tile / num_n;
+      const int n_blk = U.tile - m_blk * num_n;
       const long long m_base = static_cast<long long>(m_blk) * 256 + rank * 128 + q * 32;
+      if (U.part > 0) {
+        // split-K part: this warp's raw accumulator (32 rows x 128 columns) to the scratch as
+        // [column quad][lane] float4, then one release arrival on the owner warp's counter
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t t_part = tmem_base + ((q * 32u) << 16) + acc * BN + col0;
+        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<char*>(epi.sk_ws) + kSkFlagBytes) +
+                      static_cast<size_t>(((U.tail * (sk_s - 1) + U.part - 1) * 2 + rank) * Cfg::kWarps + ew) *
+                          (kSkWarpFloats / 4) +
+                      lane;
+#pragma unroll 1
+        for (int g = 0; g < BN / kSplit / 32; ++g) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_part + 32 * g, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            stcg_f4(dst + (g * 8 + j) * 32, make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                                        __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3])));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive_remote(tempty_leader0 + acc * 8);
+          __threadfence();
+          int* flags = reinterpret_cast<int*>(epi.sk_ws);
+          red_release_gpu_add(flags + (U.tail * 2 + rank) * Cfg::kWarps + ew, 1);
+        }
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        continue;
+      }
       // kResidTma: the residual box c (32 rows x 32 fp32 of this warp's columns) goes by TMA
       // into staging box c & 1, once that box's previous store has read it; box 0 before the
       // accumulator wait, box c + 1 while box c is finished.
@@ -792,6 +852,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
+          }
+          if (U.tail >= 0) {  // split-K owner: add parts 1 .. s - 1 of these columns, in order
+            if (c == 0) {
+              if (lane == 0) {
+                int* f = reinterpret_cast<int*>(epi.sk_ws) +
+                         (U.tail * 2 + rank) * Cfg::kWarps + ew;
+                while (ld_acquire_gpu(f) < sk_s - 1) __nanosleep(32);
+                *f = 0;  // (every part has arrived: the next launch starts from zero)
+              }
+              __syncwarp();
+            }
+            const float4* src = reinterpret_cast<const float4*>(reinterpret_cast<const char*>(epi.sk_ws) + kSkFlagBytes) +
+                                static_cast<size_t>((U.tail * (sk_s - 1) * 2 + rank) * Cfg::kWarps + ew) *
+                                    (kSkWarpFloats / 4) +
+                                (c * CW / 4) * 32 + lane;
+#pragma unroll 1
+            for (int p = 1; p < sk_s; ++p) {
+              const float4* sp = src + static_cast<size_t>(p - 1) * 2 * Cfg::kWarps * (kSkWarpFloats / 4);
+#pragma unroll
+              for (int j = 0; j < CW / 4; ++j) {
+                const float4 a = ldcg_f4(sp + j * 32);
+                v[4 * j] += a.x;
+                v[4 * j + 1] += a.y;
+                v[4 * j + 2] += a.z;
+                v[4 * j + 3] += a.w;
+              }
+            }
           }
           if (epi.skip == 1) return false;
           if (epi.skip >= 4 && static_cast<int>(q) == epi.skip - 4) return false;  // profiling: one lane quarter's warps idle
@@ -1289,6 +1376,30 @@ int make_tmap_attn_out(CUtensorMap* map, const void* base, uint64_t images, uint
   return r == CUDA_SUCCESS ? TA_OK : TA_ERR_SHAPE;
 }
 
+// Split-K tail parts for a launch of `tiles` pair tiles over `pairs` clusters (1 = no split):
+// the R = tiles % pairs tiles of the last wave are cut into s = min(pairs / R, TA_GEMM_SPLITK
+// (default 4)) parts of at least 4 k-blocks each, for K >= TA_GEMM_SK_MINKB k-blocks (default
+// 24: fc2; a 12-k-block tile's tail costs less than the partial round trip would save).
+static int splitk_parts(int tiles, int pairs, int num_kb, bool have_ws) {
+  static const int max_parts = [] {
+    const char* v = getenv("TA_GEMM_SPLITK");
+    return v ? atoi(v) : 4;
+  }();
+  static const int min_kb = [] {
+    const char* v = getenv("TA_GEMM_SK_MINKB");
+    return v ? atoi(v) : 24;
+  }();
+  const int R = tiles % pairs;
+  if (!have_ws || max_parts < 2 || num_kb < min_kb || R == 0) return 1;
+  int p = std::min(std::min(pairs / R, max_parts), num_kb / 4);
+  if (static_cast<size_t>(R) * 2 * 8 * 4 > kSkFlagBytes) p = 1;
+  return p >= 2 ? p : 1;
+}
+
+size_t gemm_splitk_flag_bytes() { return kSkFlagBytes; }
+// partials: R (s - 1) < pairs tiles' worth, 256 x 256 fp32 each
+size_t gemm_splitk_ws_bytes() { return kSkFlagBytes + static_cast<size_t>(device_sm_count() / 2) * 256 * 256 * 4; }
+
 template <int EPI, typename OutT, bool kRemap = false, int kVar = 0>
 static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, int N, int K,
                        const GemmEpi& epi, cudaStream_t stream) {
@@ -1319,8 +1430,12 @@ static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
   }
   const int tiles = ((M + 255) / 256) * (N / 256);
   const int pairs = device_sm_count() / 2;
+  GemmEpi e = epi;
+  e.sk_split = splitk_parts(tiles, pairs, K / kBK, epi.sk_ws != nullptr);
+  e.sk_full = e.sk_split > 1 ? tiles - tiles % pairs : tiles;
+  const int units = e.sk_full + (tiles - e.sk_full) * e.sk_split;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * (tiles < pairs ? tiles : pairs));
+  cfg.gridDim = dim3(2 * (units < pairs ? units : pairs));
   cfg.blockDim = dim3(Cfg::kThreads);
   cfg.dynamicSmemBytes = Cfg::kSmemBytes;
   cfg.stream = stream;
@@ -1329,8 +1444,8 @@ static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta_, tb_, tc_, tr_, tx_, M, N, K, epi);
-  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
+  cudaError_t ce = cudaLaunchKernelEx(&cfg, kern, ta_, tb_, tc_, tr_, tx_, M, N, K, e);
+  return ce == cudaSuccess ? TA_OK : set_last_cuda_error(ce);
 }
 
 // Residual + statistics GEMMs with K <= kShortK (proj, fused proj + merge) store the bf16 copy

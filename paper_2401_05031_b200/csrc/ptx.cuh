@@ -306,6 +306,19 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* ptr, uint32_t bytes
                : "memory");
 }
 
+// GPU-scope flag handshake between CTAs (split-K partials): release add / acquire load.
+__device__ __forceinline__ void red_release_gpu_add(int* ptr, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
+// L2-coherent 16-byte load / store (data another SM wrote / will read in this launch)
+__device__ __forceinline__ float4 ldcg_f4(const float4* p) { return __ldcg(p); }
+__device__ __forceinline__ void stcg_f4(float4* p, float4 v) { __stcg(p, v); }
+
 // ---------------------------------------------------------------- tcgen05
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {

@@ -217,3 +217,29 @@ def test_merge_fusion_matches_merge_kernel(tmp_path):
         # the one-warp-per-source fixup against the per-source chain kernel, same forced trace
         c = torch.load(tmp_path / f"fusion1c_g{gamma}.pt")
         assert (fb - _finite(c["forced"])).abs().max().item() <= BF16_TOL * scale
+
+
+def test_splitk_forward(tmp_path):
+    """Split-K tail tiles in the forward's GEMMs (TA_GEMM_SPLITK_FWD=1; off by default because a
+    row's summation order then depends on its batch position) against the default, with the
+    same forced trace: logits within the bf16 bound, and run to run bit for bit (the owner adds
+    the parts in a fixed order)."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    for flag in ("0", "1"):
+        env = dict(os.environ, TA_GEMM_SPLITK_FWD=flag)
+        r = subprocess.run([sys.executable, os.path.join(here, "splitk_check.py"), str(tmp_path)],
+                           env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+    for gamma in (-16, 0, 8):
+        a = torch.load(tmp_path / f"sk0_g{gamma}.pt")
+        b = torch.load(tmp_path / f"sk1_g{gamma}.pt")
+        fa, fb = _finite(a["forced"]), _finite(b["forced"])
+        scale = fa.abs().max().item()
+        assert (fa - fb).abs().max().item() <= BF16_TOL * scale
+        assert not torch.equal(fa, fb)  # the split ran (different fp32 summation order)
+        for run in (a, b):
+            assert torch.equal(run["forced"], run["again"])

@@ -32,7 +32,11 @@ def _chk(rc):
 
 
 @pytest.mark.parametrize("m,n,k", [(1, 768, 768), (127, 384, 768), (300, 2304, 768),
-                                   (1000, 768, 3072), (50432 // 8, 3072, 768)])
+                                   (1000, 768, 3072), (50432 // 8, 3072, 768),
+                                   # split-K tails (gemm.cu splitk_parts): 240 tiles -> 18 x 4 parts,
+                                   # 159 -> 11 x 4, ragged M 237 -> 15 x 4, 30 tiles -> 2 parts
+                                   (20480, 768, 3072), (13568, 768, 3072), (20000, 768, 2048),
+                                   (1280, 1536, 3072)])
 @pytest.mark.parametrize("epi", [0, 1, 2])
 def test_gemm_bf16_tcgen05(L, m, n, k, epi):
     g = torch.Generator(device="cuda").manual_seed(m + n + k + epi)
