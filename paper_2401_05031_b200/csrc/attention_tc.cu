@@ -69,7 +69,7 @@ struct AttnTcLayout {
   int nkc_last; // 16-key PV steps of the last block (chunks [nch_last, 2 nkc_last) are zeros)
   int n_kb;     // t_pad / 64
   int n_qt;     // ceil(t / 128)
-  int n_kv;     // K/V ring slots (2 when t_pad <= 256)
+  int n_kv;     // K/V ring slots (4 when t_pad <= 128 and they fit, 2 when t_pad <= 256)
   int n_s;      // TMEM S slots (2 when t_pad <= 256)
   int rowsplit; // 1: softmax group g owns every other tile (t_pad <= 128); 0: groups split keys
   int o_col;    // single S slot with O in its own TMEM columns [o_col, o_col + hd) (0: O aliases S)
@@ -126,6 +126,13 @@ AttnTcLayout attn_layout(int t, int hd) {
   L.kv_bytes = L.vt_off + L.n_kb * L.tail_blk;
   // hd = 80 at t_pad = 256: two K/V slots would not fit beside Q and the P ring
   if (L.n_kv == 2 && L.q_bytes + 2 * L.kv_bytes + 4 * kPBytes + 8192 > 227u * 1024) L.n_kv = 1;
+  // One-tile items (t_pad <= 128): a tile's softmax is short next to a K / V load, so with two
+  // slots the next item's load (issued when a PV releases a slot) sat on the critical path
+  // (trace at t = 69: 3100 clk from O committed to the group's next S); four slots load two
+  // items ahead.  TA_ATTN_KV=2 keeps two (profiling A/B).
+  if (L.t_pad <= 128 && L.q_bytes + 4 * L.kv_bytes + 4 * kPBytes + 8192 <= 227u * 1024) L.n_kv = 4;
+  if (const char* e = getenv("TA_ATTN_KV"))
+    if (e[0] == '2' && L.n_kv == 4) L.n_kv = 2;
   uint32_t off = (L.q_bytes + 1023) / 1024 * 1024;  // Q: one slot (Q(n+1) is only needed after S(n))
   L.kv_off = off;
   off += L.n_kv * L.kv_bytes;
@@ -136,7 +143,7 @@ AttnTcLayout attn_layout(int t, int hd) {
   L.red_off = off;
   off += 4 * 128 * 4;
   L.bar_off = off;
-  off += 32 * 8;
+  off += 40 * 8;
   L.smem_bytes = off + 1024;  // + alignment slack
   return L;
 }
@@ -193,8 +200,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // K and V of an item have separate lifetimes: K is free once the item's last S MMA is done,
   // V after its last PV, so with one K/V slot the next item's K (and first S) need not wait
   // for the PV tail of the previous item.
-  uint64_t* kv_full = bars + 0;   // [2] K of the slot landed
-  uint64_t* kv_free = bars + 2;   // [2] K of the slot consumed
+  uint64_t* kv_full = bars + 32;  // [4] K of the slot landed
+  uint64_t* kv_free = bars + 36;  // [4] K of the slot consumed
   uint64_t* v_full = bars + 22;   // [2]
   uint64_t* v_free = bars + 24;   // [2]
   uint64_t* q_full = bars + 4;    // [2]
@@ -211,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // No runtime integer division in the loops below: it compiles to I2F / MUFU.RCP / F2I on
   // the SFU, which the softmax exponentials saturate on every sub-partition, and the MMA
   // issuer then waited ~700 cycles per P block.  Items advance by gridDim.x as (b, h) pairs;
-  // ring indices use n_kv, n_s in {1, 2}.
+  // ring indices use n_kv in {1, 2, 4}, n_s in {1, 2}.
   const int step_b = static_cast<int>(gridDim.x) / H;
   const int step_h = static_cast<int>(gridDim.x) - step_b * H;
   const int b_first = static_cast<int>(blockIdx.x) / H;
@@ -224,15 +231,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++b;
     }
   };
-  auto ring_slot = [](uint32_t x, int n) -> uint32_t { return n == 2 ? (x & 1u) : 0u; };
-  auto ring_use = [](uint32_t x, int n) -> uint32_t { return n == 2 ? (x >> 1) : x; };
+  auto ring_slot = [](uint32_t x, int n) -> uint32_t { return x & static_cast<uint32_t>(n - 1); };
+  auto ring_use = [](uint32_t x, int n) -> uint32_t { return n == 4 ? (x >> 2) : n == 2 ? (x >> 1) : x; };
   if (warp == 8 && lane == 0) {
     tma_prefetch(&tm);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < 4; ++s) {
       // row split: every tile of an item releases its K / V (MMA warp 9 or 10, one per tile)
-      const int rel = L.rowsplit ? L.n_qt : 1;
       mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_free[s], rel);
+      mbar_init(&kv_free[s], L.rowsplit ? L.n_qt : 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      const int rel = L.rowsplit ? L.n_qt : 1;
       mbar_init(&v_full[s], 1);
       mbar_init(&v_free[s], rel);
       mbar_init(&q_full[s], 1);

@@ -550,6 +550,8 @@ struct PairCfg {
   static constexpr int kXhBytes = kXh ? kWarps * 2 * 2048 : 0;
   static constexpr int kStages = kXh ? 4 : (kEpiBytes > 32768 || kLnSmem) ? 5 : 6;
   static constexpr int kSmemBytes = kStages * kStageBytes + kEpiBytes + kLnBytes + kXhBytes + 1024 + 512;
+  // split-K tail code compiled in for the ta_gemm kinds and the long-K residual GEMM (fc2) only
+  static constexpr bool kSplitK = kVar == 2 || EPI == EPI_BIAS || EPI == EPI_BIAS_GELU || EPI == EPI_BIAS_RESID;
 };
 
 // Split-K tail.  When the last wave of 256 x 256 tiles would leave most clusters idle, the
@@ -639,8 +641,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
   const int num_kb = K / kBK;
   const int cid = static_cast<int>(cluster_id_x());
   const int ncl = static_cast<int>(nclusters_x());
-  const int sk_s = epi.sk_split, sk_full = epi.sk_full;
+  const int sk_s = Cfg::kSplitK ? epi.sk_split : 1;
+  const int sk_full = Cfg::kSplitK ? epi.sk_full : num_tiles;
   const int num_units = sk_full + (num_tiles - sk_full) * sk_s;
+  auto unit_of = [&](int u) { return Cfg::kSplitK ? sk_unit(u, sk_full, sk_s, num_kb) : SkUnit{u, 0, num_kb, 0, -1}; };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -648,7 +652,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
       int stage = 0;
       uint32_t phase = 0;
       for (int unit = cid; unit < num_units; unit += ncl) {
-        const SkUnit U = sk_unit(unit, sk_full, sk_s, num_kb);
+        const SkUnit U = unit_of(unit);
         const int m_blk = U.tile / num_n;
         const int n_blk = U.tile - m_blk * num_n;
         for (int kb = U.kb0; kb < U.kb1; ++kb) {
@@ -677,7 +681,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int unit = cid; unit < num_units; unit += ncl) {
-        const SkUnit U = sk_unit(unit, sk_full, sk_s, num_kb);
+        const SkUnit U = unit_of(unit);
         mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base_u + acc * BN;
@@ -718,11 +722,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
     uint32_t r_par = 0u;  // kResidTma: bit b = mbarrier parity of staging box b's next load
     const bool resid_tma = Cfg::kResidTma && !epi.resid_ldg;
     for (int unit = cid; unit < num_units; unit += ncl) {
-      const SkUnit U = sk_unit(unit, sk_full, sk_s, num_kb);
+      const SkUnit U = unit_of(unit);
       const int m_blk = U.tile / num_n;
       const int n_blk = U.tile - m_blk * num_n;
       const long long m_base = static_cast<long long>(m_blk) * 256 + rank * 128 + q * 32;
-      if (U.part > 0) {
+      if (Cfg::kSplitK && U.part > 0) {
         // split-K part: this warp's raw accumulator (32 rows x 128 columns) to the scratch as
         // [column quad][lane] float4, then one release arrival on the owner warp's counter
         mbar_wait(&tfull[acc], acc_phase);
@@ -853,7 +857,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
           }
-          if (U.tail >= 0) {  // split-K owner: add parts 1 .. s - 1 of these columns, in order
+          if (Cfg::kSplitK && U.tail >= 0) {  // split-K owner: add parts 1 .. s - 1 of these columns, in order
             if (c == 0) {
               if (lane == 0) {
                 int* f = reinterpret_cast<int*>(epi.sk_ws) +
@@ -1431,7 +1435,7 @@ static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
   const int tiles = ((M + 255) / 256) * (N / 256);
   const int pairs = device_sm_count() / 2;
   GemmEpi e = epi;
-  e.sk_split = splitk_parts(tiles, pairs, K / kBK, epi.sk_ws != nullptr);
+  e.sk_split = Cfg::kSplitK ? splitk_parts(tiles, pairs, K / kBK, epi.sk_ws != nullptr) : 1;
   e.sk_full = e.sk_split > 1 ? tiles - tiles % pairs : tiles;
   const int units = e.sk_full + (tiles - e.sk_full) * e.sk_split;
   cudaLaunchConfig_t cfg = {};
