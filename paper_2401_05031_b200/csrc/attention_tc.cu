@@ -174,10 +174,12 @@ __device__ __forceinline__ int q_order(int qt, uint32_t item_local, const AttnTc
   return (L.qswap && (item_local & 1u)) ? 1 - qt : qt;
 }
 
-// kOne: one K/V slot (L.n_kv == 1), where K and V have separate barriers and lifetimes and a
+// kOne (kKv == 1): one K/V slot, where K and V have separate barriers and lifetimes and a
 // single S slot may keep O in its own TMEM columns (L.o_col); a template parameter so that the
 // two-slot instance carries none of that state (its register budget is tight).
-template <bool kHasSize, int kHD, bool kOne>
+// kKv: K/V ring slots (L.n_kv), a template parameter so that the one- and two-slot instances
+// compile as before the four-slot ring (a runtime slot count cost them ~2 %).
+template <bool kHasSize, int kHD, int kKv>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmt,
                    const __grid_constant__ CUtensorMap tmo,
@@ -188,6 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
+  constexpr bool kOne = kKv == 1;
   constexpr int kTail = kHD - kHd;  // 16-column SW32 tail of a head_dim = 80 row (0 for 64)
   const uint32_t o_col = kOne ? static_cast<uint32_t>(L.o_col) : 0u;
   const int D = H * kHD;
@@ -200,8 +203,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // K and V of an item have separate lifetimes: K is free once the item's last S MMA is done,
   // V after its last PV, so with one K/V slot the next item's K (and first S) need not wait
   // for the PV tail of the previous item.
-  uint64_t* kv_full = bars + 32;  // [4] K of the slot landed
-  uint64_t* kv_free = bars + 36;  // [4] K of the slot consumed
+  uint64_t* kv_full = bars + (kKv == 4 ? 32 : 0);  // [kKv] K of the slot landed
+  uint64_t* kv_free = bars + (kKv == 4 ? 36 : 2);  // [kKv] K of the slot consumed
   uint64_t* v_full = bars + 22;   // [2]
   uint64_t* v_free = bars + 24;   // [2]
   uint64_t* q_full = bars + 4;    // [2]
@@ -231,11 +234,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++b;
     }
   };
-  auto ring_slot = [](uint32_t x, int n) -> uint32_t { return x & static_cast<uint32_t>(n - 1); };
-  auto ring_use = [](uint32_t x, int n) -> uint32_t { return n == 4 ? (x >> 2) : n == 2 ? (x >> 1) : x; };
+  auto ring_slot = [](uint32_t x, int n) -> uint32_t { return n == 2 ? (x & 1u) : 0u; };
+  auto ring_use = [](uint32_t x, int n) -> uint32_t { return n == 2 ? (x >> 1) : x; };
+  // K/V ring of kKv slots
+  auto kv_slot = [](uint32_t x) -> int { return static_cast<int>(x & static_cast<uint32_t>(kKv - 1)); };
+  auto kv_round = [](uint32_t x) -> uint32_t { return kKv == 4 ? (x >> 2) : kKv == 2 ? (x >> 1) : x; };
   if (warp == 8 && lane == 0) {
     tma_prefetch(&tm);
-    for (int s = 0; s < 4; ++s) {
+    for (int s = 0; s < kKv; ++s) {
       // row split: every tile of an item releases its K / V (MMA warp 9 or 10, one per tile)
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_free[s], L.rowsplit ? L.n_qt : 1);
@@ -275,8 +281,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int b = b_first, h = h_first;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it, next_bh(b, h)) {
         const int row_base = b * t;
-        const int kvs = ring_slot(it, L.n_kv);
-        const uint32_t kv_use = ring_use(it, L.n_kv);
+        const int kvs = kv_slot(it);
+        const uint32_t kv_use = kv_round(it);
         mbar_wait(&kv_free[kvs], (kv_use & 1) ^ 1);
         uint8_t* sK = sKV + kvs * L.kv_bytes;
         uint8_t* sV = sK + L.n_kb * kBlkBytes;
@@ -294,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         };
 #ifdef TA_ATTN_EXP_KVONCE  // profiling only: wrong results (K / V of the first items reused)
-        if (it >= static_cast<uint32_t>(L.n_kv) && !split_v) {
+        if (it >= static_cast<uint32_t>(kKv) && !split_v) {
           mbar_arrive(&kv_full[kvs]);
         } else
 #endif
@@ -411,8 +417,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t o_tmem = slot_tmem + static_cast<uint32_t>(L.o_sep);
         uint32_t j = 0, pu = 0, n = 0, it = 0;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-          const int kvs = ring_slot(it, L.n_kv);
-          const uint32_t kv_par = ring_use(it, L.n_kv) & 1;
+          const int kvs = kv_slot(it);
+          const uint32_t kv_par = kv_round(it) & 1;
           const uint8_t* sKVslot = sKV + kvs * L.kv_bytes;
           for (int qt = 0; qt < L.n_qt; ++qt, ++n) {
             if ((n & 1u) != g) continue;
@@ -463,8 +469,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else if (warp == 9) {
       uint32_t it = 0, qcnt = 0, tcnt = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        const int kvs = ring_slot(it, L.n_kv);
-        const uint32_t kv_use = ring_use(it, L.n_kv);
+        const int kvs = kv_slot(it);
+        const uint32_t kv_use = kv_round(it);
         const uint8_t* sK = sKV + kvs * L.kv_bytes;
         for (int qt = 0; qt < L.n_qt; ++qt, ++qcnt, ++tcnt) {
           const int ss = ring_slot(tcnt, L.n_s);
@@ -771,19 +777,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 int make_tmap_bf16_2d_sw(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                          uint32_t box_cols, uint32_t box_rows, int swizzle_bytes);
 
-template <bool kHasSize, int kHD, bool kOne>
+template <bool kHasSize, int kHD, int kKv>
 static cudaError_t launch_attn_tc(const cudaLaunchConfig_t& cfg, const CUtensorMap& tm,
                                   const CUtensorMap& tmt, const CUtensorMap& tmo, const float* size,
                                   int t, int H, int n_items, __nv_bfloat16* o, float scale_log2,
                                   const AttnTcLayout& L) {
   static unsigned long long attr_mask = 0;  // per instantiation and device
   if (attr_needed(attr_mask)) {
-    const cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<kHasSize, kHD, kOne>,
+    const cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<kHasSize, kHD, kKv>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr_done(attr_mask);
   }
-  return cudaLaunchKernelEx(&cfg, attn_tc_kernel<kHasSize, kHD, kOne>, tm, tmt, tmo, size, t, H, n_items, o,
+  return cudaLaunchKernelEx(&cfg, attn_tc_kernel<kHasSize, kHD, kKv>, tm, tmt, tmo, size, t, H, n_items, o,
                             scale_log2, L);
 }
 
@@ -819,14 +825,18 @@ int attention_tc(const void* qkv, const float* size, int B, int t, int H, int hd
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(hd));
   auto* o = static_cast<__nv_bfloat16*>(out);
   cudaError_t e;
-#define TA_ATTN_LAUNCH(S, HD, ONE) launch_attn_tc<S, HD, ONE>(cfg, tm, tmt, tmo, size, t, H, n_items, o, scale_log2, L)
-  const bool one = L.n_kv == 1, sz = size != nullptr;
-  if (hd == 64)
-    e = one ? (sz ? TA_ATTN_LAUNCH(true, 64, true) : TA_ATTN_LAUNCH(false, 64, true))
-            : (sz ? TA_ATTN_LAUNCH(true, 64, false) : TA_ATTN_LAUNCH(false, 64, false));
+#define TA_ATTN_LAUNCH(S, HD, KV) launch_attn_tc<S, HD, KV>(cfg, tm, tmt, tmo, size, t, H, n_items, o, scale_log2, L)
+  const bool sz = size != nullptr;
+  if (hd == 64 && L.n_kv == 4)
+    e = sz ? TA_ATTN_LAUNCH(true, 64, 4) : TA_ATTN_LAUNCH(false, 64, 4);
+  else if (hd == 64)
+    e = L.n_kv == 1 ? (sz ? TA_ATTN_LAUNCH(true, 64, 1) : TA_ATTN_LAUNCH(false, 64, 1))
+                    : (sz ? TA_ATTN_LAUNCH(true, 64, 2) : TA_ATTN_LAUNCH(false, 64, 2));
+  else if (L.n_kv <= 2)
+    e = L.n_kv == 1 ? (sz ? TA_ATTN_LAUNCH(true, 80, 1) : TA_ATTN_LAUNCH(false, 80, 1))
+                    : (sz ? TA_ATTN_LAUNCH(true, 80, 2) : TA_ATTN_LAUNCH(false, 80, 2));
   else
-    e = one ? (sz ? TA_ATTN_LAUNCH(true, 80, true) : TA_ATTN_LAUNCH(false, 80, true))
-            : (sz ? TA_ATTN_LAUNCH(true, 80, false) : TA_ATTN_LAUNCH(false, 80, false));
+    return TA_ERR_SHAPE;  // (hd 80 never gets four slots: they do not fit)
 #undef TA_ATTN_LAUNCH
   return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }

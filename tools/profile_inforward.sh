@@ -26,6 +26,7 @@ cap proj_merge_inforward -8 'pair_kernel<\(int\)8' 2  # fused proj + merge (scat
 cap fixup_inforward -8 'merge_fixup' 2
 cap attn_t197_inforward 0 'attn_tc_kernel' 2
 cap attn_t389_inforward 16 'attn_tc_kernel' 11
+cap attn_t117_inforward -16 'attn_tc_kernel' 5    # one-tile items (four K/V slots), layer 5
 cap match_bf16_inforward -8 'match_fused_kernel' 2
 cap patchify_inforward 0 'patchify' 0
 cap head_inforward 0 'head_kernel' 0
