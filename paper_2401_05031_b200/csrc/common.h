@@ -68,12 +68,6 @@ struct GemmEpi {
   // rows [rows_out, M) the merged-away source tokens (image b's k-th source at rows_out + b r + k),
   // which merge_fixup folds into their destinations.
   const int32_t* row_map = nullptr;
-  // Split-K tail (CTA-pair kernel): scratch for the partial accumulators of the last wave's
-  // tiles (gemm_splitk_ws_bytes(): fp32 partials, then per-warp arrival counters that must be
-  // zero before the first launch and are left zero by every launch).  Null: no split.
-  float* sk_ws = nullptr;
-  int sk_split = 1;                 // set by the launcher: parts per tail tile
-  int sk_full = 0;                  // set by the launcher: tiles before the tail
   int skip = 0;                     // profiling only (TA_GEMM_SKIP_EPILOGUE=1): no epilogue work
   int direct_store = 0;             // TA_GEMM_STORE=direct: STG.256 rows instead of TMA boxes
   int resid_ldg = 0;                // TA_GEMM_RESID=ldg: residual rows by per-thread loads
@@ -116,11 +110,13 @@ struct HeadDesc {
 };
 
 // Launchers (gemm.cu)
+// sk_ws: split-K tail scratch (gemm_splitk_ws_bytes(); null: no split).  Not a GemmEpi field:
+// growing that struct changed the generated code of every GEMM instance (fc1 +1.8 %).
 int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, bool out_bf16,
-              const GemmEpi& epi, cudaStream_t stream);
+              const GemmEpi& epi, cudaStream_t stream, float* sk_ws = nullptr);
 int gemm_f32(const float* A, const float* W, int M, int N, int K, int epi_kind,
              const GemmEpi& epi, cudaStream_t stream);
-// Split-K tail scratch for gemm_bf16 (GemmEpi::sk_ws): its first gemm_splitk_flag_bytes() are
+// Split-K tail scratch for gemm_bf16 (sk_ws): its first gemm_splitk_flag_bytes() are
 // counters the owner zeroes once (cudaMemsetAsync) before the first GEMM that uses it.
 size_t gemm_splitk_ws_bytes();
 size_t gemm_splitk_flag_bytes();

@@ -219,11 +219,10 @@ Workspace carve(const ta_model* m, int B, const Schedule& s, char* base) {
 int linear(const ta_model* m, const void* a, const void* wt, int M, int N, int K, int epi_kind,
            const GemmEpi& epi_in, cudaStream_t st, const Workspace& w) {
   void* const tf32_scratch = w.tf32_scratch;
-  GemmEpi epi = epi_in;
-  epi.sk_ws = w.sk_ws;
+  const GemmEpi& epi = epi_in;
   if (m->d.dtype == TA_DTYPE_BF16)
     return gemm_bf16(a, wt, M, N, K, epi_kind, epi_kind == EPI_BIAS || epi_kind == EPI_BIAS_GELU || epi_is_ln(epi_kind),
-                     epi, st);
+                     epi, st, w.sk_ws);
   if (f32_gemm_backend() == 0)
     return gemm_f32_tc(static_cast<const float*>(a), static_cast<const float*>(wt), M, N, K, epi_kind, epi,
                        tf32_scratch, st);
@@ -802,8 +801,7 @@ int ta_gemm(const void* a, const void* w, const float* bias, const float* resid,
     if (ce != cudaSuccess) return set_last_cuda_error(ce);
     ce = cudaMemsetAsync(sk, 0, gemm_splitk_flag_bytes(), st);
     if (ce != cudaSuccess) return set_last_cuda_error(ce);
-    e.sk_ws = static_cast<float*>(sk);
-    const int rc = gemm_bf16(a, w, m, n, k, epilogue, out_dtype == TA_DTYPE_BF16, e, st);
+    const int rc = gemm_bf16(a, w, m, n, k, epilogue, out_dtype == TA_DTYPE_BF16, e, st, static_cast<float*>(sk));
     cudaFreeAsync(sk, st);
     return rc;
   }

@@ -571,6 +571,11 @@ __device__ __forceinline__ SkUnit sk_unit(int u, int full, int s, int num_kb) {
   const int i = u - full, t = i / s, p = i - t * s;
   return {full + t, p * num_kb / s, (p + 1) * num_kb / s, p, t};
 }
+struct SplitK {
+  float* ws;  // counters (kSkFlagBytes), then partials
+  int split;  // parts per tail tile (1: no split)
+  int full;   // tiles before the tail
+};
 constexpr int kSkWarpFloats = 32 * 128;  // one epilogue warp's partial: 32 rows x 128 columns
 // scratch layout: counters first (room for 256 tail tiles x 2 CTAs x 8 warps), then partials
 constexpr size_t kSkFlagBytes = 256 * 2 * 8 * 4;
@@ -582,7 +587,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
                                 const __grid_constant__ CUtensorMap tmC,
                                 const __grid_constant__ CUtensorMap tmR,
                                 const __grid_constant__ CUtensorMap tmX, int M, int N, int K,
-                                GemmEpi epi) {
+                                GemmEpi epi, SplitK sk) {
   using Cfg = PairCfg<EPI, OutT, kRemap, kVar>;
   constexpr int BN = 256;
   constexpr int S = Cfg::kStages;
@@ -641,9 +646,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
   const int num_kb = K / kBK;
   const int cid = static_cast<int>(cluster_id_x());
   const int ncl = static_cast<int>(nclusters_x());
-  const int sk_s = Cfg::kSplitK ? epi.sk_split : 1;
-  const int sk_full = Cfg::kSplitK ? epi.sk_full : num_tiles;
-  const int num_units = sk_full + (num_tiles - sk_full) * sk_s;
+  const int sk_s = Cfg::kSplitK ? sk.split : 1;
+  const int sk_full = Cfg::kSplitK ? sk.full : num_tiles;
+  const int num_units = Cfg::kSplitK ? sk_full + (num_tiles - sk_full) * sk_s : num_tiles;
   auto unit_of = [&](int u) { return Cfg::kSplitK ? sk_unit(u, sk_full, sk_s, num_kb) : SkUnit{u, 0, num_kb, 0, -1}; };
 
   if (warp == 0) {
@@ -694,7 +699,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           const uint64_t bdesc = umma_desc_sw128(sb);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
-            umma_f16_pair_w(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, ((kb - U.kb0) | k) != 0);
+            umma_f16_pair_w(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc,
+                            ((Cfg::kSplitK ? kb - U.kb0 : kb) | k) != 0);
           umma_commit_pair_w(&empty[stage]);
           if (++stage == S) {
             stage = 0;
@@ -732,7 +738,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const uint32_t t_part = tmem_base + ((q * 32u) << 16) + acc * BN + col0;
-        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<char*>(epi.sk_ws) + kSkFlagBytes) +
+        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<char*>(sk.ws) + kSkFlagBytes) +
                       static_cast<size_t>(((U.tail * (sk_s - 1) + U.part - 1) * 2 + rank) * Cfg::kWarps + ew) *
                           (kSkWarpFloats / 4) +
                       lane;
@@ -751,7 +757,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
         if (lane == 0) {
           mbar_arrive_remote(tempty_leader0 + acc * 8);
           __threadfence();
-          int* flags = reinterpret_cast<int*>(epi.sk_ws);
+          int* flags = reinterpret_cast<int*>(sk.ws);
           red_release_gpu_add(flags + (U.tail * 2 + rank) * Cfg::kWarps + ew, 1);
         }
         if (++acc == 2) {
@@ -860,14 +866,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<EPI, OutT, k
           if (Cfg::kSplitK && U.tail >= 0) {  // split-K owner: add parts 1 .. s - 1 of these columns, in order
             if (c == 0) {
               if (lane == 0) {
-                int* f = reinterpret_cast<int*>(epi.sk_ws) +
+                int* f = reinterpret_cast<int*>(sk.ws) +
                          (U.tail * 2 + rank) * Cfg::kWarps + ew;
                 while (ld_acquire_gpu(f) < sk_s - 1) __nanosleep(32);
                 *f = 0;  // (every part has arrived: the next launch starts from zero)
               }
               __syncwarp();
             }
-            const float4* src = reinterpret_cast<const float4*>(reinterpret_cast<const char*>(epi.sk_ws) + kSkFlagBytes) +
+            const float4* src = reinterpret_cast<const float4*>(reinterpret_cast<const char*>(sk.ws) + kSkFlagBytes) +
                                 static_cast<size_t>((U.tail * (sk_s - 1) * 2 + rank) * Cfg::kWarps + ew) *
                                     (kSkWarpFloats / 4) +
                                 (c * CW / 4) * 32 + lane;
@@ -1406,7 +1412,7 @@ size_t gemm_splitk_ws_bytes() { return kSkFlagBytes + static_cast<size_t>(device
 
 template <int EPI, typename OutT, bool kRemap = false, int kVar = 0>
 static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, int N, int K,
-                       const GemmEpi& epi, cudaStream_t stream) {
+                       const GemmEpi& epi, cudaStream_t stream, float* sk_ws) {
   using Cfg = PairCfg<EPI, OutT, kRemap, kVar>;
   auto kern = gemm_bf16_sm100_pair_kernel<EPI, OutT, kRemap, kVar>;
   static unsigned long long attr_mask = 0;  // per instantiation and device
@@ -1434,10 +1440,10 @@ static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
   }
   const int tiles = ((M + 255) / 256) * (N / 256);
   const int pairs = device_sm_count() / 2;
-  GemmEpi e = epi;
-  e.sk_split = Cfg::kSplitK ? splitk_parts(tiles, pairs, K / kBK, epi.sk_ws != nullptr) : 1;
-  e.sk_full = e.sk_split > 1 ? tiles - tiles % pairs : tiles;
-  const int units = e.sk_full + (tiles - e.sk_full) * e.sk_split;
+  SplitK sk{sk_ws, 1, tiles};
+  sk.split = Cfg::kSplitK ? splitk_parts(tiles, pairs, K / kBK, sk_ws != nullptr) : 1;
+  sk.full = sk.split > 1 ? tiles - tiles % pairs : tiles;
+  const int units = sk.full + (tiles - sk.full) * sk.split;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * (units < pairs ? units : pairs));
   cfg.blockDim = dim3(Cfg::kThreads);
@@ -1448,8 +1454,8 @@ static int launch_pair(const CUtensorMap& ta_, const CUtensorMap& tb_, int M, in
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled();
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t ce = cudaLaunchKernelEx(&cfg, kern, ta_, tb_, tc_, tr_, tx_, M, N, K, e);
-  return ce == cudaSuccess ? TA_OK : set_last_cuda_error(ce);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta_, tb_, tc_, tr_, tx_, M, N, K, epi, sk);
+  return e == cudaSuccess ? TA_OK : set_last_cuda_error(e);
 }
 
 // Residual + statistics GEMMs with K <= kShortK (proj, fused proj + merge) store the bf16 copy
@@ -1474,40 +1480,40 @@ static bool xh_tma_enabled() {
 }
 
 static int dispatch_pair(const CUtensorMap& a, const CUtensorMap& b, int M, int N, int K,
-                         int epi_kind, bool out_bf16, const GemmEpi& epi, cudaStream_t s) {
+                         int epi_kind, bool out_bf16, const GemmEpi& epi, cudaStream_t s, float* sk_ws) {
   switch (epi_kind) {
     case EPI_BIAS:
-      return out_bf16 ? launch_pair<EPI_BIAS, __nv_bfloat16>(a, b, M, N, K, epi, s)
-                      : launch_pair<EPI_BIAS, float>(a, b, M, N, K, epi, s);
+      return out_bf16 ? launch_pair<EPI_BIAS, __nv_bfloat16>(a, b, M, N, K, epi, s, sk_ws)
+                      : launch_pair<EPI_BIAS, float>(a, b, M, N, K, epi, s, sk_ws);
     case EPI_BIAS_GELU:
-      return out_bf16 ? launch_pair<EPI_BIAS_GELU, __nv_bfloat16>(a, b, M, N, K, epi, s)
-                      : launch_pair<EPI_BIAS_GELU, float>(a, b, M, N, K, epi, s);
+      return out_bf16 ? launch_pair<EPI_BIAS_GELU, __nv_bfloat16>(a, b, M, N, K, epi, s, sk_ws)
+                      : launch_pair<EPI_BIAS_GELU, float>(a, b, M, N, K, epi, s, sk_ws);
     case EPI_BIAS_RESID:
       if (K >= kLongK && one_box_enabled())
-        return epi.rows_in ? launch_pair<EPI_BIAS_RESID, float, true, 2>(a, b, M, N, K, epi, s)
-                           : launch_pair<EPI_BIAS_RESID, float, false, 2>(a, b, M, N, K, epi, s);
-      return epi.rows_in ? launch_pair<EPI_BIAS_RESID, float, true>(a, b, M, N, K, epi, s)
-                         : launch_pair<EPI_BIAS_RESID, float, false>(a, b, M, N, K, epi, s);
+        return epi.rows_in ? launch_pair<EPI_BIAS_RESID, float, true, 2>(a, b, M, N, K, epi, s, sk_ws)
+                           : launch_pair<EPI_BIAS_RESID, float, false, 2>(a, b, M, N, K, epi, s, sk_ws);
+      return epi.rows_in ? launch_pair<EPI_BIAS_RESID, float, true>(a, b, M, N, K, epi, s, sk_ws)
+                         : launch_pair<EPI_BIAS_RESID, float, false>(a, b, M, N, K, epi, s, sk_ws);
     case EPI_PATCH:
-      return launch_pair<EPI_PATCH, float, true>(a, b, M, N, K, epi, s);
+      return launch_pair<EPI_PATCH, float, true>(a, b, M, N, K, epi, s, sk_ws);
     case EPI_BIAS_RESID_STATS:
       if (K >= kLongK && one_box_enabled())
-        return epi.rows_in ? launch_pair<EPI_BIAS_RESID_STATS, float, true, 2>(a, b, M, N, K, epi, s)
-                           : launch_pair<EPI_BIAS_RESID_STATS, float, false, 2>(a, b, M, N, K, epi, s);
-      if (epi.rows_in) return launch_pair<EPI_BIAS_RESID_STATS, float, true>(a, b, M, N, K, epi, s);
+        return epi.rows_in ? launch_pair<EPI_BIAS_RESID_STATS, float, true, 2>(a, b, M, N, K, epi, s, sk_ws)
+                           : launch_pair<EPI_BIAS_RESID_STATS, float, false, 2>(a, b, M, N, K, epi, s, sk_ws);
+      if (epi.rows_in) return launch_pair<EPI_BIAS_RESID_STATS, float, true>(a, b, M, N, K, epi, s, sk_ws);
       return K <= kShortK && xh_tma_enabled()
-                 ? launch_pair<EPI_BIAS_RESID_STATS, float, false, 1>(a, b, M, N, K, epi, s)
-                 : launch_pair<EPI_BIAS_RESID_STATS, float, false>(a, b, M, N, K, epi, s);
+                 ? launch_pair<EPI_BIAS_RESID_STATS, float, false, 1>(a, b, M, N, K, epi, s, sk_ws)
+                 : launch_pair<EPI_BIAS_RESID_STATS, float, false>(a, b, M, N, K, epi, s, sk_ws);
     case EPI_PATCH_STATS:
-      return launch_pair<EPI_PATCH_STATS, float, true>(a, b, M, N, K, epi, s);
+      return launch_pair<EPI_PATCH_STATS, float, true>(a, b, M, N, K, epi, s, sk_ws);
     case EPI_LN_BIAS:
-      return launch_pair<EPI_LN_BIAS, __nv_bfloat16>(a, b, M, N, K, epi, s);
+      return launch_pair<EPI_LN_BIAS, __nv_bfloat16>(a, b, M, N, K, epi, s, sk_ws);
     case EPI_LN_GELU:
-      return launch_pair<EPI_LN_GELU, __nv_bfloat16>(a, b, M, N, K, epi, s);
+      return launch_pair<EPI_LN_GELU, __nv_bfloat16>(a, b, M, N, K, epi, s, sk_ws);
     case EPI_BIAS_RESID_MERGE:
       // (the merge kind keeps the per-thread bf16 stores: 16 scatter4 per box on a 4-stage ring
       // measured 81.5 -> 87.5 us per fused proj)
-      return launch_pair<EPI_BIAS_RESID_MERGE, float, false>(a, b, M, N, K, epi, s);
+      return launch_pair<EPI_BIAS_RESID_MERGE, float, false>(a, b, M, N, K, epi, s, sk_ws);
   }
   return TA_ERR_INVALID;
 }
@@ -1551,7 +1557,7 @@ static int dispatch_bf16(const CUtensorMap& a, const CUtensorMap& b, int M, int 
 }
 
 int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, bool out_bf16,
-              const GemmEpi& epi_in, cudaStream_t stream) {
+              const GemmEpi& epi_in, cudaStream_t stream, float* sk_ws) {
   static const int skip_epi = [] {
     // profiling only: 1 = mainloop + TMEM drain only, 2 = no TMA store
     const char* v = getenv("TA_GEMM_SKIP_EPILOGUE");
@@ -1594,7 +1600,7 @@ int gemm_bf16(const void* A, const void* W, int M, int N, int K, int epi_kind, b
   if (BN == 256 && gemm_backend() == 0) {
     rc = make_tmap_bf16_2d(&tb_, W, N, K, 128);  // each CTA of the pair loads 128 W rows
     if (rc) return rc;
-    return dispatch_pair(ta_, tb_, M, N, K, epi_kind, out_bf16, epi, stream);
+    return dispatch_pair(ta_, tb_, M, N, K, epi_kind, out_bf16, epi, stream, sk_ws);
   }
   rc = make_tmap_bf16_2d(&tb_, W, N, K, BN);
   if (rc) return rc;
