@@ -20,7 +20,9 @@ chk = _cuda.check
 
 # GEMMs: single-CTA kernel (M <= 3072 and N <= 1024) and the CTA-pair kernel (M = 4000 and
 # N = 2048; the residual kind reads its residual boxes by TMA), epilogues 0 / 1 / 2
-for M, N, K in ((300, 512, 128), (97, 256, 192), (1000, 768, 256), (4000, 768, 256), (3300, 2048, 128)):
+# (1280 x 1536 x 3072: 30 tiles in 2 split-K parts; 6912 x 768 x 3072: 81 tiles, the last 7 in 4 parts)
+for M, N, K in ((300, 512, 128), (97, 256, 192), (1000, 768, 256), (4000, 768, 256), (3300, 2048, 128),
+                (1280, 1536, 3072), (6912, 768, 3072)):
     a = torch.randn(M, K, device=dev).bfloat16()
     w = (torch.randn(N, K, device=dev) * 0.05).bfloat16()
     bias = torch.randn(N, device=dev)
@@ -31,7 +33,8 @@ for M, N, K in ((300, 512, 128), (97, 256, 192), (1000, 768, 256), (4000, 768, 2
     out = torch.empty(M, N, device=dev)
     chk(lib.ta_gemm(a.data_ptr(), w.data_ptr(), bias.data_ptr(), resid.data_ptr(), out.data_ptr(), M, N, K, 2, 0, 1, st))
 # attention at a few token counts, with and without the size vector
-for b, t, H, hd in ((2, 53, 12, 64), (2, 197, 12, 64), (1, 300, 12, 64), (1, 257, 16, 80)):
+# (64 x 117: one-tile items on the four-slot K/V ring, > 4 items per CTA so the ring wraps)
+for b, t, H, hd in ((2, 53, 12, 64), (2, 197, 12, 64), (64, 117, 12, 64), (1, 300, 12, 64), (1, 257, 16, 80)):
     qkv = torch.randn(b * t, 3 * H * hd, device=dev).bfloat16()
     size = torch.randint(1, 4, (b, t), device=dev).float()
     out = torch.empty(b * t, H * hd, device=dev, dtype=torch.bfloat16)
