@@ -60,8 +60,11 @@ struct AttnCfg {
   static constexpr int kSmem = (kBQ + 4 * kBK) * kLd * 2 + 2 * kBK * 4;
 };
 
+// hd 64: capped at 128 registers (no spills) for four CTAs per SM instead of three -- the kernel
+// runs the t <= 64 tail layers of the merge schedules and is latency-bound: t = 21 / 37 / 53 / 64
+// 23.3 / 24.0 / 26.3 / 30.5 -> 20.6 / 21.6 / 24.0 / 27.0 us (B = 256, H = 12).  hd 80 would spill.
 template <int HD>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, HD == 64 ? 4 : 1)
     attn_bf16_kernel(const __nv_bfloat16* __restrict__ qkv, const float* __restrict__ size,
                      int t, int H, __nv_bfloat16* __restrict__ out, float scale_log2) {
   using C = AttnCfg<HD>;
