@@ -43,6 +43,7 @@ from .batcher import BatchingThresholds, BatchQueue
 from .core import Batch, OutcomeType, Query, TokenPlan, classify_outcome, us_from_s
 from .errors import ConfigError
 from .profiles import MemoryModel, ProfileTable, estimate_batch
+from .replicas import next_free
 
 __all__ = ["EngineConfig", "SimReport", "TableExecutor", "GpuExecutor", "AsyncGpuExecutor",
            "AsyncTableExecutor", "ServingEngine", "arrival_rate", "DEFAULT_TASKS", "synthetic_accuracy",
@@ -352,7 +353,7 @@ class ServingEngine:
             rep.events.append((finish - lat, "execute", batch.id, replica, gamma, lat, util))
 
         while True:
-            r_i = min(range(n_rep), key=lambda i: (free_at[i], i))
+            r_i = next_free(free_at)
             now = free_at[r_i]
             if not queue.batches:
                 if nxt >= len(qs):

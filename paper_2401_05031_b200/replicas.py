@@ -17,7 +17,7 @@ import subprocess
 import sys
 from typing import List, Optional, Sequence, Tuple
 
-__all__ = ["round_robin", "earliest_free", "aggregate_throughput", "launch_replicas", "free_port"]
+__all__ = ["round_robin", "earliest_free", "next_free", "aggregate_throughput", "launch_replicas", "free_port"]
 
 
 def round_robin(n_batches: int, world: int) -> List[List[int]]:
@@ -28,6 +28,14 @@ def round_robin(n_batches: int, world: int) -> List[List[int]]:
     for i in range(n_batches):
         out[i % world].append(i)
     return out
+
+
+def next_free(free_at_us: Sequence[int]) -> int:
+    """The replica that frees up first (ties -> lowest replica id): the dispatch rule of
+    ``earliest_free`` for one batch, used by the serving engine (engine.py)."""
+    if not free_at_us:
+        raise ValueError("no replicas")
+    return min(range(len(free_at_us)), key=lambda i: (free_at_us[i], i))
 
 
 def earliest_free(costs_us: Sequence[int], world: int,

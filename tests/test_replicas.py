@@ -18,6 +18,15 @@ def test_round_robin():
         replicas.round_robin(3, 0)
 
 
+def test_next_free():
+    from paper_2401_05031_b200.replicas import next_free
+
+    assert next_free([5, 3, 3, 9]) == 1
+    assert next_free([0]) == 0
+    with pytest.raises(ValueError):
+        next_free([])
+
+
 def test_earliest_free():
     assign, finish = replicas.earliest_free([100, 50, 50, 10, 200], 2)
     assert assign == [[0, 3], [1, 2, 4]]
