@@ -154,6 +154,23 @@ def test_attention_batched_tails(L, t, with_size, ramp):
     torch.testing.assert_close(out.double(), ref, rtol=2e-2, atol=2e-2)
 
 
+@pytest.mark.parametrize("t", [69, 117, 128])
+@pytest.mark.parametrize("with_size", [False, True])
+def test_attention_kv_ring_wraps(L, t, with_size):
+    """One-tile items (t <= 128) on the four-slot K/V ring with > 4 items per CTA (B = 80, H = 12:
+    960 items over at most 148 CTAs), so every slot is reused several times."""
+    b, heads, hd = 80, 12, 64
+    g = torch.Generator(device="cuda").manual_seed(2000 + t)
+    qkv = (torch.randn(b, t, 3 * heads * hd, device="cuda", generator=g) * 2).bfloat16()
+    size = (torch.randint(1, 9, (b, t), device="cuda", generator=g).float() if with_size else None)
+    out = torch.empty(b, t, heads * hd, device="cuda", dtype=torch.bfloat16)
+    _chk(L.ta_attention(qkv.data_ptr(), size.data_ptr() if size is not None else None, b, t, heads, hd,
+                        out.data_ptr(), 0, _s()))
+    torch.cuda.synchronize()
+    ref = _attn_ref(qkv.float(), size, b, t, heads, hd)
+    torch.testing.assert_close(out.double(), ref, rtol=2e-2, atol=2e-2)
+
+
 @pytest.mark.parametrize("t,r", [(197, 8), (197, 16), (189, 8), (21, 10), (3, 1), (257, 24), (4, 1)])
 @pytest.mark.parametrize("c", [64, 80])
 def test_match_bit_exact(L, t, r, c):
