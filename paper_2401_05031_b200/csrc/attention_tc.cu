@@ -48,6 +48,16 @@ int make_tmap_attn_out(CUtensorMap* map, const void* base, uint64_t images, uint
 
 namespace {
 
+// Barrier waits of the TMA producer carry a suspend-time hint (mbar_wait_sleep), so its polling
+// takes fewer issue slots from the softmax warps of its sub-partition: t = 197 104.0 -> 102.6 us,
+// t = 117 45.4 -> 44.9 us (B = 256, two interleaved runs).  Build flag for A/B: -DTA_ATTN_WAIT_SLEEP=0
+// plain try_wait loops, =2 the MMA warps' waits too (no better than 1).
+#ifndef TA_ATTN_WAIT_SLEEP
+#define TA_ATTN_WAIT_SLEEP 1
+#endif
+#define PWAIT(b, p) (TA_ATTN_WAIT_SLEEP >= 1 ? mbar_wait_sleep((b), (p), 1000) : mbar_wait((b), (p)))
+#define MWAIT(b, p) (TA_ATTN_WAIT_SLEEP >= 2 ? mbar_wait_sleep((b), (p), 1000) : mbar_wait((b), (p)))
+
 constexpr int kHd = 64;
 constexpr int kQTile = 128;
 constexpr int kKeyBlk = 64;
@@ -283,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row_base = b * t;
         const int kvs = kv_slot(it);
         const uint32_t kv_use = kv_round(it);
-        mbar_wait(&kv_free[kvs], (kv_use & 1) ^ 1);
+        PWAIT(&kv_free[kvs], (kv_use & 1) ^ 1);
         uint8_t* sK = sKV + kvs * L.kv_bytes;
         uint8_t* sV = sK + L.n_kb * kBlkBytes;
         TRACE(1);
@@ -320,9 +330,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           // reloaded once S of tile n - 1 (the other warp's) is done.  Key split: one pair.
           uint64_t* qf = &q_full[L.rowsplit ? (qcnt & 1) : 0];
           if (L.rowsplit) {
-            if (qcnt > 0) mbar_wait(&q_free[(qcnt - 1) & 1], ((qcnt - 1) >> 1) & 1);
+            if (qcnt > 0) PWAIT(&q_free[(qcnt - 1) & 1], ((qcnt - 1) >> 1) & 1);
           } else {
-            mbar_wait(&q_free[0], (qcnt & 1) ^ 1);
+            PWAIT(&q_free[0], (qcnt & 1) ^ 1);
           }
 #ifdef TA_ATTN_EXP_QONCE  // profiling only: wrong results (Q of the first tile reused)
           if (qcnt > 0) { mbar_arrive(qf); continue; }
@@ -338,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           TRACE(2);
           if (qt == 0 && split_v) {
-            mbar_wait(&v_free[kvs], (kv_use & 1) ^ 1);
+            PWAIT(&v_free[kvs], (kv_use & 1) ^ 1);
             mbar_arrive_expect_tx(&v_full[kvs], half_bytes);
             load_v(&v_full[kvs]);
           }
@@ -385,14 +395,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_pv = [&](int sslot, int kvs, bool last_of_item, bool first_of_item, uint32_t v_par) {
         const uint8_t* sKVslot = sKV + kvs * L.kv_bytes;
         const uint32_t o_tmem = o_col ? tmem + o_col : tmem + sslot * 256;
-        if (first_of_item && kOne) mbar_wait(&v_full[kvs], v_par);
+        if (first_of_item && kOne) MWAIT(&v_full[kvs], v_par);
         for (int kb = 0; kb < L.n_kb; ++kb) {
           const int grp = kb & 1;
           const uint32_t u = p_use[grp]++;
           const int ps = 2 * grp + (u & 1);
-          mbar_wait(&p_full[ps], (u >> 1) & 1);
+          MWAIT(&p_full[ps], (u >> 1) & 1);
           if (kTail > 0 && kb == 0 && L.n_kb > 1 && !o_col)  // O[0, 80) overlaps S block 1: wait for its P
-            mbar_wait(&p_full[2 + (p_use[1] & 1)], (p_use[1] >> 1) & 1);
+            MWAIT(&p_full[2 + (p_use[1] & 1)], (p_use[1] >> 1) & 1);
           TRACE(5);
           tc_fence_after();
           const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
@@ -422,9 +432,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint8_t* sKVslot = sKV + kvs * L.kv_bytes;
           for (int qt = 0; qt < L.n_qt; ++qt, ++n) {
             if ((n & 1u) != g) continue;
-            mbar_wait(&s_free[g], (j & 1) ^ 1);  // group g has read O of its previous tile
-            mbar_wait(&q_full[g], j & 1);
-            mbar_wait(&kv_full[kvs], kv_par);
+            MWAIT(&s_free[g], (j & 1) ^ 1);  // group g has read O of its previous tile
+            MWAIT(&q_full[g], j & 1);
+            MWAIT(&kv_full[kvs], kv_par);
             TRACE(7);
             tc_fence_after();
             {
@@ -442,16 +452,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_commit_w(&q_free[g]);
             if (kOne) umma_commit_w(&kv_free[kvs]);  // this tile's use of K is done
             TRACE(4);
-            if (kOne) mbar_wait(&v_full[kvs], kv_par);
-            if (L.o_sep && j > 0) mbar_wait(&o_free[g], (j - 1) & 1);  // O of the previous tile read
+            if (kOne) MWAIT(&v_full[kvs], kv_par);
+            if (L.o_sep && j > 0) MWAIT(&o_free[g], (j - 1) & 1);  // O of the previous tile read
             for (int kb = 0; kb < L.n_kb; ++kb) {
               const int ps = 2 * g + (pu & 1);
-              mbar_wait(&p_full[ps], (pu >> 1) & 1);
+              MWAIT(&p_full[ps], (pu >> 1) & 1);
               ++pu;
               // head_dim 80 with O in the slot: O[0, 80) overlaps S block 1, so block 0's PV waits
               // for block 1's P
               if (kTail > 0 && kb == 0 && L.n_kb > 1 && !L.o_sep)
-                mbar_wait(&p_full[2 * g + (pu & 1)], (pu >> 1) & 1);
+                MWAIT(&p_full[2 * g + (pu & 1)], (pu >> 1) & 1);
               TRACE(8 + 16 * g);
               tc_fence_after();
               const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
@@ -478,9 +488,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             issue_pv(pend_slot, pend_kvs, pend_last, pend_first, pend_vpar);
             pend_slot = -1;
           }
-          mbar_wait(&s_free[ss], (ring_use(tcnt, L.n_s) & 1) ^ 1);
-          mbar_wait(&q_full[0], qcnt & 1);
-          if (qt == 0) mbar_wait(&kv_full[kvs], kv_use & 1);
+          MWAIT(&s_free[ss], (ring_use(tcnt, L.n_s) & 1) ^ 1);
+          MWAIT(&q_full[0], qcnt & 1);
+          if (qt == 0) MWAIT(&kv_full[kvs], kv_use & 1);
           TRACE(3);
           tc_fence_after();
           const uint64_t qdesc = umma_desc_sw128(smem_u32(sQ));
