@@ -1,10 +1,12 @@
-"""bench.py's reference arm on CPU (the driver runs it on the GPU box as `bench.py --impl reference`):
-one JSON line with the contract's keys, and ranks > 0 of a multi-rank launch exit 0 without work.
-ViT-tiny, two gammas, two images per gamma, so the whole test takes seconds."""
+"""bench.py's JSON contract.  CPU: the reference arm (the driver runs it on the GPU box as `bench.py
+--impl reference`) prints one line with the contract's keys, and ranks > 0 of a multi-rank launch exit
+0 without work (ViT-tiny, two gammas, two images per gamma: seconds).  GPU: our arm on ViT-tiny."""
 import json
 import os
 import subprocess
 import sys
+
+import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ARGS = ["--impl", "reference", "--steps", "1", "--warmup", "0", "--model", "vit_tiny", "--gammas=-4,0",
@@ -40,3 +42,24 @@ def test_reference_arm_other_ranks_exit_quietly():
     r = _run({"RANK": "1", "LOCAL_RANK": "1", "WORLD_SIZE": "2"})
     assert r.returncode == 0, r.stderr[-2000:]
     assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+
+
+@pytest.mark.gpu
+def test_our_arm_json_line():
+    """The GPU arm on a small model: the contract's keys, device-timed value, e2e with real copies,
+    roofline / clocks / gpu_launches present."""
+    env = dict(os.environ)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--model", "vit_tiny", "--batch", "16",
+                        "--steps", "3", "--warmup", "3", "--no-cpu", "--no-fp32", "--gammas=-4,0"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")]
+    d = json.loads(lines[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "dtype", "data", "config", "e2e", "roofline", "clocks", "gpu_launches"):
+        assert k in d, k
+    assert d["value"] > 0 and d["steps"] == 3 and d["warmup"] == 3 and d["gpu_launches"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    for k in ("bound", "achieved", "peak", "unit", "frac"):
+        assert k in d["roofline"], k
+    assert "sm_mhz" in d["clocks"]
