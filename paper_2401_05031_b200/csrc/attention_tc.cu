@@ -77,6 +77,8 @@ struct AttnTcLayout {
   int t_mma;    // round_up(t, 16): S MMA N (keys past it are never read)
   int nch_last; // 8-key chunks of the last 64-key block holding keys < t
   int nkc_last; // 16-key PV steps of the last block (chunks [nch_last, 2 nkc_last) are zeros)
+  int mtail;    // row split, hd 64: the last block's <= 16 keys ride with the previous P block
+  int n_pb;     // P blocks per tile (n_kb - mtail)
   int n_kb;     // t_pad / 64
   int n_qt;     // ceil(t / 128)
   int n_kv;     // K/V ring slots (4 when t_pad <= 128 and they fit, 2 when t_pad <= 256)
@@ -86,7 +88,7 @@ struct AttnTcLayout {
   int qswap;    // row split, two query tiles: odd items take their tiles in reverse order
   int o_sep;    // row split: O in its own columns [256 g + o_sep, 256 g + 256) of slot g (0: aliases S)
   uint32_t kv_bytes;  // per slot: K then V
-  uint32_t kv_off, p_off, bias_off, red_off, bar_off, smem_bytes;
+  uint32_t kv_off, p_off, mt_off, bias_off, red_off, bar_off, smem_bytes;
 };
 
 AttnTcLayout attn_layout(int t, int hd) {
@@ -148,6 +150,19 @@ AttnTcLayout attn_layout(int t, int hd) {
   off += L.n_kv * L.kv_bytes;
   L.p_off = off;
   off += 4 * kPBytes;  // P ring: two stages per softmax group
+  // Merged tail (row split, hd 64, last key block holding <= 16 keys, e.g. t = 197 / 205 / 133 / 69):
+  // those keys' P goes to a 128 x 16 SW32 tile of the group (4 KB) written with the previous
+  // 64-key block and taken by the same PV step as one more K = 16 MMA, so a tile walks n_kb - 1
+  // P-ring stages instead of n_kb (TA_ATTN_MTAIL=0 keeps the separate last block).
+  L.mtail = 0;
+  {
+    const int rem = t - (L.n_kb - 1) * kKeyBlk;
+    const char* e = getenv("TA_ATTN_MTAIL");
+    if (L.rowsplit && L.tail == 0 && L.n_kb >= 2 && rem <= 16 && !(e && e[0] == '0')) L.mtail = 1;
+  }
+  L.n_pb = L.n_kb - L.mtail;
+  L.mt_off = off;
+  if (L.mtail) off += 2 * 4096;
   L.bias_off = off;
   off += kMaxTPad * 4;
   L.red_off = off;
@@ -454,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             TRACE(4);
             if (kOne) MWAIT(&v_full[kvs], kv_par);
             if (L.o_sep && j > 0) MWAIT(&o_free[g], (j - 1) & 1);  // O of the previous tile read
-            for (int kb = 0; kb < L.n_kb; ++kb) {
+            for (int kb = 0; kb < L.n_pb; ++kb) {
               const int ps = 2 * g + (pu & 1);
               MWAIT(&p_full[ps], (pu >> 1) & 1);
               ++pu;
@@ -467,6 +482,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t pdesc = umma_desc_sw128(smem_u32(sP + ps * kPBytes));
               const int nkc = kb == L.n_kb - 1 ? L.nkc_last : kKeyBlk / 16;
               pv_block(std::true_type{}, o_tmem, pdesc, sKVslot, kb, nkc);
+              if (kTail == 0 && L.mtail && kb == L.n_pb - 1)  // the merged tail: keys 64 (n_kb - 1) + [0, 16)
+                pv_block(std::true_type{}, o_tmem, umma_desc_sw32(smem_u32(smem + L.mt_off + g * 4096)), sKVslot,
+                         L.n_kb - 1, 1);
               umma_commit_w(&p_free[ps]);
               TRACE(5 + 16 * g);
             }
@@ -666,7 +684,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           drain_o_store();
           uint64_t acc[2] = {0ull, 0ull};
           const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(nmx, nmx);
-          for (int kb = 0; kb < L.n_kb; ++kb, ++use) {
+          for (int kb = 0; kb < L.n_pb; ++kb, ++use) {
             const bool last = kb == L.n_kb - 1;
             uint32_t r[64];
             if (!idle) {
@@ -684,6 +702,21 @@ __global__ void __launch_bounds__(kThreads, 1)
               else
                 softmax_block_tail(r, sc2, nm2, s_bias_g + kb * 64 * 4, s_prow, i, L.nch_last,
                                    2 * L.nkc_last, acc);
+              if (kTail == 0 && L.mtail && kb == L.n_pb - 1) {
+                // merged tail: this row's keys 64 (n_kb - 1) + [0, 16) into the group's SW32 tile
+                // (16-byte chunk c of row i at c ^ ((i >> 2) & 1)); weights are 0 past t
+                uint32_t rt[16];
+                tmem_ld_32x32b_x16(la + (L.n_kb - 1) * 64, rt);
+                tmem_ld_wait();
+                const uint32_t s_mt = smem_u32(smem + L.mt_off) + g * 4096u + static_cast<uint32_t>(i) * 32u;
+                const uint32_t s_wt = s_bias_g + (L.n_kb - 1) * 64 * 4;
+                const uint32_t sw = (static_cast<uint32_t>(i) >> 2) & 1u;
+                uint4 v0 = softmax_chunk8<TA_ATTN_POLY_EVEN>(&rt[0], sc2, nm2, true, s_wt, acc);
+                uint4 v1 = make_uint4(0u, 0u, 0u, 0u);
+                if (L.nch_last > 1) v1 = softmax_chunk8<TA_ATTN_POLY_ODD>(&rt[8], sc2, nm2, true, s_wt + 32, acc);
+                sts_u4(s_mt + (sw << 4), v0);
+                sts_u4(s_mt + ((1u ^ sw) << 4), v1);
+              }
               fence_proxy_async_smem();
             }
             tc_fence_before();  // S reads done before the PV MMA may overwrite block 0
